@@ -1,0 +1,1164 @@
+// C-ABI implementation of the bidomain PCG hot path (see include/bidomain_b200.h).
+//
+// One private non-blocking stream per context; every public call orders
+// itself after the caller's stream with an event and hands back with another,
+// so callers see plain stream semantics while the PCG loop can be captured
+// into a CUDA graph (conditional WHILE node) on the private stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bidomain_b200.h"
+#include "bd_device.cuh"
+#include "bd_host.hpp"
+
+using namespace bd;
+using dev::Ctl;
+
+#define BD_VERSION "bidomain_b200 0.1 sm_100a"
+
+struct bd_ctx {
+  int device = 0;
+  cudaStream_t user = nullptr;    // caller's stream (may be the legacy default)
+  cudaStream_t stream = nullptr;  // private stream all work runs on
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int nsm = 148;
+  // profiling
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, int>> marks;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[8] = {0};
+  int64_t prof_launch[8] = {0};
+  // utility control block (dot / mean readbacks)
+  Ctl util{};
+  double* h_pin = nullptr;  // pinned readback scratch (64 doubles)
+};
+
+struct bd_csr {
+  bd_ctx* ctx;
+  int64_t nrows, ncols, nnz;
+  int* rowptr = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;
+  int G = 8;
+  dev::Csr dev() const { return dev::Csr{(int)nrows, rowptr, col, val}; }
+};
+
+struct DevTri {
+  int n = 0;
+  int* rowptr = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;
+  int* tasks = nullptr;
+  int ntasks = 0;
+  int nvb = 0;
+  int64_t depth = 0;
+  int64_t nnz = 0;
+  dev::Tri dev() const { return dev::Tri{n, rowptr, col, val, tasks, ntasks}; }
+};
+
+struct bd_inner {
+  bd_ctx* ctx;
+  int kind;
+  int64_t n;
+  int G = 8;
+  DevTri L, U;
+  int* perm = nullptr;        // exact: new -> old
+  double* inv = nullptr;      // jacobi
+  double* y_int = nullptr;    // forward output (sentinel between solves)
+  double* x_int = nullptr;    // internal backward output for standalone / exact
+  HostCsr hlower;
+  std::vector<int32_t> hperm;
+  int restarts = 0;
+  Ctl ctl{};                  // standalone control block
+};
+
+struct bd_system {
+  bd_ctx* ctx;
+  bd_csr* S1;
+  bd_csr* Si;
+  int64_t n, m;
+  double* mass = nullptr;
+  double* mh = nullptr;
+  double gamma;
+  Ctl ctl{};
+  double* tmp = nullptr;  // n+m scratch
+};
+
+struct bd_prec {
+  bd_system* sys;
+  bd_inner* bulk;
+  bd_inner* schur;
+  double beta;
+  int64_t cnt[3] = {0, 0, 0};
+  Ctl ctl{};       // PCG control block (flags on)
+  Ctl ctl_nf{};    // same storage, flags off (standalone applies, final normalise)
+  double *traw, *z2raw, *corr, *sbuf;  // P^{-1} scratch
+  double *x, *r, *z, *d, *q;           // PCG vectors (n+m)
+  int hist_cap = 0;
+  // CUDA graph of one PCG iteration inside a WHILE node
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr;
+  bool use_graph = true;
+};
+
+// ---------------------------------------------------------------------------
+namespace {
+
+bd_status fail(bd_ctx* ctx, bd_status st, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+#define CK(ctx, expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail((ctx), BD_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_));  \
+  } while (0)
+
+#define LAUNCHED(ctx)                                                                   \
+  do {                                                                                  \
+    (ctx)->launches++;                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return fail((ctx), BD_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, int64_t count) {
+  return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1));
+}
+
+int grid_for(bd_ctx* ctx, int64_t items, int per_block) {
+  const int64_t need = (items + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)ctx->nsm * 8));
+}
+
+int pick_g(double avg) {
+  int g = 4;
+  while (g < 32 && g < avg) g <<= 1;
+  return g;
+}
+
+// Caller-stream handoff.
+struct Scope {
+  bd_ctx* c;
+  explicit Scope(bd_ctx* ctx) : c(ctx) {
+    cudaEventRecord(c->ev_in, c->user);
+    cudaStreamWaitEvent(c->stream, c->ev_in, 0);
+  }
+  ~Scope() {
+    cudaEventRecord(c->ev_out, c->stream);
+    cudaStreamWaitEvent(c->user, c->ev_out, 0);
+  }
+};
+
+void prof_mark(bd_ctx* ctx, int cls) {
+  if (!ctx->profile) return;
+  cudaEvent_t e;
+  if (ctx->pool.empty()) {
+    cudaEventCreate(&e);
+  } else {
+    e = ctx->pool.back();
+    ctx->pool.pop_back();
+  }
+  cudaEventRecord(e, ctx->stream);
+  ctx->marks.push_back({e, cls});
+  ctx->prof_launch[cls]++;
+}
+
+void prof_collect(bd_ctx* ctx) {
+  if (ctx->marks.size() < 2) {
+    for (auto& m : ctx->marks) ctx->pool.push_back(m.first);
+    ctx->marks.clear();
+    return;
+  }
+  cudaEventSynchronize(ctx->marks.back().first);
+  for (size_t i = 1; i < ctx->marks.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->marks[i - 1].first, ctx->marks[i].first);
+    ctx->prof_ms[ctx->marks[i].second] += ms;
+  }
+  for (auto& m : ctx->marks) ctx->pool.push_back(m.first);
+  ctx->marks.clear();
+}
+
+cudaError_t ctl_alloc(Ctl* c, int64_t partials, int hist_cap, int use_flags) {
+  cudaError_t e;
+  if ((e = dalloc(&c->sc, dev::NSLOTS))) return e;
+  if ((e = dalloc(&c->fl, dev::NFLAGS))) return e;
+  if ((e = dalloc(&c->partials, std::max<int64_t>(partials, 4096) * 2))) return e;
+  if ((e = dalloc(&c->ctr, dev::NCTR))) return e;
+  if ((e = cudaMemset(c->sc, 0, sizeof(double) * dev::NSLOTS))) return e;
+  if ((e = cudaMemset(c->fl, 0, sizeof(int) * dev::NFLAGS))) return e;
+  if ((e = cudaMemset(c->ctr, 0, sizeof(unsigned) * dev::NCTR))) return e;
+  c->hist_cap = hist_cap;
+  if (hist_cap > 0) {
+    if ((e = dalloc(&c->res_hist, hist_cap))) return e;
+    if ((e = dalloc(&c->prec_hist, hist_cap))) return e;
+  } else {
+    c->res_hist = c->prec_hist = nullptr;
+  }
+  c->use_flags = use_flags;
+  return cudaSuccess;
+}
+
+void ctl_free(Ctl* c, bool own_hist = true) {
+  cudaFree(c->sc);
+  cudaFree(c->fl);
+  cudaFree(c->partials);
+  cudaFree(c->ctr);
+  if (own_hist) {
+    cudaFree(c->res_hist);
+    cudaFree(c->prec_hist);
+  }
+}
+
+// ---- device Tri upload ------------------------------------------------------
+bd_status upload_tri(bd_ctx* ctx, const HostCsr& t, bool lower, int G, DevTri* out) {
+  std::vector<int32_t> level;
+  out->depth = row_levels(t, lower, &level);
+  std::vector<int32_t> tasks;
+  build_schedule(level, out->depth, 32 / G, &tasks);
+  out->n = (int)t.n;
+  out->nnz = t.nnz();
+  out->ntasks = (int)tasks.size();
+  out->nvb = (int)((tasks.size() + (dev::TPB / G) - 1) / (dev::TPB / G));
+  std::vector<int> rp(t.n + 1);
+  for (int64_t i = 0; i <= t.n; ++i) rp[i] = (int)t.indptr[i];
+  CK(ctx, dalloc(&out->rowptr, t.n + 1));
+  CK(ctx, dalloc(&out->col, t.nnz()));
+  CK(ctx, dalloc(&out->val, t.nnz()));
+  CK(ctx, dalloc(&out->tasks, (int64_t)tasks.size()));
+  CK(ctx, cudaMemcpy(out->rowptr, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice));
+  CK(ctx, cudaMemcpy(out->col, t.indices.data(), sizeof(int) * t.nnz(), cudaMemcpyHostToDevice));
+  CK(ctx, cudaMemcpy(out->val, t.values.data(), sizeof(double) * t.nnz(), cudaMemcpyHostToDevice));
+  CK(ctx, cudaMemcpy(out->tasks, tasks.data(), sizeof(int) * tasks.size(), cudaMemcpyHostToDevice));
+  return BD_OK;
+}
+
+void free_tri(DevTri* t) {
+  cudaFree(t->rowptr);
+  cudaFree(t->col);
+  cudaFree(t->val);
+  cudaFree(t->tasks);
+}
+
+// ---- inner solve dispatch -----------------------------------------------------
+// Solve P x = rhs for one inner preconditioner inside control block c.
+// x_int: polled internal output (sentinel-filled here); out (nullable):
+// scatter target in the original ordering; fin/slot/slot2: optional mean of
+// the output.
+template <int G, class Rhs>
+bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out, const Ctl& c,
+                        int ctr0, int fin, int slot, int slot2, int64_t nmean) {
+  bd_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  if (p->kind == BD_INNER_JACOBI) {
+    const int grid = grid_for(ctx, p->n, dev::TPB / G);
+    dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
+                                                      ctr0, fin, slot, slot2, nmean);
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
+  dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(x_int, p->n, dev::SENTINEL, c);
+  LAUNCHED(ctx);
+  dev::k_trsv_fwd<G, true, Rhs><<<p->L.nvb, dev::TPB, 0, st>>>(p->L.dev(), rhs, p->y_int, c, ctr0,
+                                                               ctr0 + 1, p->L.nvb);
+  LAUNCHED(ctx);
+  dev::k_trsv_bwd<G, false><<<p->U.nvb, dev::TPB, 0, st>>>(p->U.dev(), p->y_int, x_int, out, p->perm,
+                                                           c, ctr0 + 2, ctr0 + 3, p->U.nvb, fin,
+                                                           slot, slot2, nmean);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+template <class Rhs>
+bd_status inner_solve(bd_inner* p, const Rhs& rhs, double* x_int, double* out, const Ctl& c,
+                      int ctr0, int fin = -1, int slot = 0, int slot2 = -1, int64_t nmean = 1) {
+  switch (p->G) {
+    case 4: return inner_solve_g<4>(p, rhs, x_int, out, c, ctr0, fin, slot, slot2, nmean);
+    case 8: return inner_solve_g<8>(p, rhs, x_int, out, c, ctr0, fin, slot, slot2, nmean);
+    case 16: return inner_solve_g<16>(p, rhs, x_int, out, c, ctr0, fin, slot, slot2, nmean);
+    default: return inner_solve_g<32>(p, rhs, x_int, out, c, ctr0, fin, slot, slot2, nmean);
+  }
+}
+
+// ---- operator -----------------------------------------------------------------
+bd_status launch_lambda(bd_system* s, const double* x, double* q, const Ctl& c, int with_dot) {
+  bd_ctx* ctx = s->ctx;
+  const int G = s->S1->G;
+  const int grid = grid_for(ctx, s->n, dev::TPB / G);
+  auto s1 = s->S1->dev();
+  auto si = s->Si->dev();
+#define LAMBDA_CASE(GG)                                                                       \
+  case GG:                                                                                    \
+    dev::k_lambda<GG><<<grid, dev::TPB, 0, ctx->stream>>>(s1, si, x, q, s->mh, s->gamma,      \
+                                                          (int)s->n, (int)s->m, c, with_dot); \
+    break;
+  switch (G) {
+    LAMBDA_CASE(4)
+    LAMBDA_CASE(8)
+    LAMBDA_CASE(16)
+    default:
+      dev::k_lambda<32><<<grid, dev::TPB, 0, ctx->stream>>>(s1, si, x, q, s->mh, s->gamma, (int)s->n,
+                                                            (int)s->m, c, with_dot);
+  }
+#undef LAMBDA_CASE
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, const Ctl& c,
+                     int ctr, int fin, int slot, int slot2, int64_t nmean) {
+  dev::k_dot<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(x, y, n, c, ctr, fin, slot,
+                                                                       slot2, nmean);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
+  bd_ctx* ctx = p->sys->ctx;
+  const int G = p->sys->Si->G;
+  const int grid = grid_for(ctx, p->sys->m, dev::TPB / G);
+  auto si = p->sys->Si->dev();
+  switch (G) {
+    case 4: dev::k_corr<4><<<grid, dev::TPB, 0, ctx->stream>>>(si, s, p->corr, c, p->sys->n); break;
+    case 8: dev::k_corr<8><<<grid, dev::TPB, 0, ctx->stream>>>(si, s, p->corr, c, p->sys->n); break;
+    case 16: dev::k_corr<16><<<grid, dev::TPB, 0, ctx->stream>>>(si, s, p->corr, c, p->sys->n); break;
+    default: dev::k_corr<32><<<grid, dev::TPB, 0, ctx->stream>>>(si, s, p->corr, c, p->sys->n);
+  }
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+#define TRY(expr)                 \
+  do {                            \
+    bd_status st_ = (expr);       \
+    if (st_ != BD_OK) return st_; \
+  } while (0)
+
+// P_Λ^{-1} r (bd/precond.py:298-312) with sc[MU1], sc[C1] already holding
+// mean(r_u) and mean(r_u)/beta.  zu: output u-block; zv_int: polled Schur
+// output (sentinel-filled); zv_out: nullable scatter copy of it.
+bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, double* zv_out,
+                       const Ctl& c, bool deflate_sum) {
+  bd_system* s = p->sys;
+  bd_ctx* ctx = s->ctx;
+  const int64_t n = s->n, m = s->m;
+  // t = bulk^{-1}(r_u - mu1), recentred lazily by its consumers
+  prof_mark(ctx, 5);
+  {
+    dev::RhsVec rhs{r, (int)n, c.sc + dev::S_MU1, p->bulk->perm};
+    double* xi = p->bulk->perm ? p->bulk->x_int : p->traw;
+    double* out = p->bulk->perm ? p->traw : nullptr;
+    if (p->bulk->kind == BD_INNER_JACOBI) {
+      xi = p->traw;
+      out = nullptr;
+    }
+    TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S, dev::FIN_MEAN, dev::S_MT, -1, n));
+  }
+  prof_mark(ctx, 2);
+  // s = K^{-1}(r_v - S_i t[:m])
+  {
+    dev::RhsSchur rhs{s->Si->dev(), p->traw, c.sc, r + n, p->schur->perm};
+    double* xi = zv_int;
+    double* out = zv_out;
+    if (p->schur->perm) {
+      xi = p->schur->x_int;
+      out = zv_out ? zv_out : zv_int;
+    }
+    if (p->schur->kind == BD_INNER_JACOBI) {
+      xi = zv_out ? zv_out : zv_int;
+      out = nullptr;
+    }
+    TRY(inner_solve(p->schur, rhs, xi, out, c, dev::C_SCH_S));
+  }
+  prof_mark(ctx, 3);
+  // correction = pad(S_i s); mu2 = mean(correction)
+  const double* sv = zv_out ? zv_out : zv_int;
+  TRY(launch_corr(p, sv, c));
+  prof_mark(ctx, 4);
+  {
+    dev::RhsVec rhs{p->corr, (int)m, c.sc + dev::S_MU2, p->bulk->perm};
+    double* xi = p->bulk->perm ? p->bulk->x_int : p->z2raw;
+    double* out = p->bulk->perm ? p->z2raw : nullptr;
+    if (p->bulk->kind == BD_INNER_JACOBI) {
+      xi = p->z2raw;
+      out = nullptr;
+    }
+    TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK2_S, dev::FIN_MEAN, dev::S_M2, -1, n));
+  }
+  prof_mark(ctx, 2);
+  dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      p->traw, p->z2raw, zu, n, c, deflate_sum ? 1 : 0);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 5);
+  return BD_OK;
+}
+
+// One PCG loop iteration (bd/krylov.py:100-131).
+bd_status enqueue_iteration(bd_prec* p) {
+  bd_system* s = p->sys;
+  bd_ctx* ctx = s->ctx;
+  const int64_t n = s->n, nm = s->n + s->m;
+  const Ctl& c = p->ctl;
+  TRY(launch_lambda(s, p->d, p->q, c, 1));
+  prof_mark(ctx, 0);
+  dev::k_update<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->x, p->r, p->d, p->q, n,
+                                                                           nm, c);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 1);
+  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));
+  dev::k_rho<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->r, p->z, n, nm, c);
+  LAUNCHED(ctx);
+  dev::k_dupdate<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->z, p->d, n, nm, c);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 5);
+  return BD_OK;
+}
+
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* fl) {
+  const volatile int* f = fl;
+  cudaGraphSetConditional(h, (f[dev::F_DONE] || f[dev::F_STOP]) ? 0u : 1u);
+}
+
+bd_status build_graph(bd_prec* p) {
+  bd_ctx* ctx = p->sys->ctx;
+  if (p->gexec) {
+    cudaGraphExecDestroy(p->gexec);
+    cudaGraphDestroy(p->graph);
+    p->gexec = nullptr;
+    p->graph = nullptr;
+  }
+  cudaGraph_t g;
+  CK(ctx, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(ctx, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(ctx, cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  CK(ctx, cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal));
+  const int64_t saved = ctx->launches;
+  bd_status st = enqueue_iteration(p);
+  k_loop_cond<<<1, 1, 0, ctx->stream>>>(h, p->ctl.fl);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &captured);
+  ctx->launches = saved;
+  if (st != BD_OK) return st;
+  CK(ctx, e);
+  CK(ctx, cudaGraphInstantiate(&p->gexec, g, nullptr, nullptr, 0));
+  p->graph = g;
+  return BD_OK;
+}
+
+int64_t iteration_launches(bd_prec* p) {
+  // Λ, update, 2 bulk solves + schur solve (3 kernels each, 1 for jacobi),
+  // corr, combine, rho, dupdate
+  auto per = [](bd_inner* in) { return in->kind == BD_INNER_JACOBI ? 1 : 3; };
+  return 2 + 2 * per(p->bulk) + per(p->schur) + 1 + 1 + 2;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* bd_version(void) { return BD_VERSION; }
+
+bd_status bd_ctx_create(int device, void* stream, bd_ctx** out) {
+  if (!out) return BD_EINVAL;
+  *out = nullptr;
+  bd_ctx* c = new bd_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return BD_ECUDA;
+  }
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  c->user = (cudaStream_t)stream;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMallocHost((void**)&c->h_pin, 64 * sizeof(double)) != cudaSuccess ||
+      ctl_alloc(&c->util, (int64_t)c->nsm * 8, 0, 0) != cudaSuccess) {
+    delete c;
+    return BD_ECUDA;
+  }
+  *out = c;
+  return BD_OK;
+}
+
+bd_status bd_ctx_destroy(bd_ctx* c) {
+  if (!c) return BD_OK;
+  cudaStreamSynchronize(c->stream);
+  ctl_free(&c->util);
+  for (auto& m : c->marks) cudaEventDestroy(m.first);
+  for (auto e : c->pool) cudaEventDestroy(e);
+  cudaFreeHost(c->h_pin);
+  cudaEventDestroy(c->ev_in);
+  cudaEventDestroy(c->ev_out);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return BD_OK;
+}
+
+bd_status bd_ctx_set_stream(bd_ctx* c, void* stream) {
+  if (!c) return BD_EINVAL;
+  c->user = (cudaStream_t)stream;
+  return BD_OK;
+}
+
+bd_status bd_ctx_synchronize(bd_ctx* c) {
+  if (!c) return BD_EINVAL;
+  CK(c, cudaStreamSynchronize(c->stream));
+  return BD_OK;
+}
+
+const char* bd_last_error(bd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t bd_launch_count(bd_ctx* c) { return c ? c->launches : 0; }
+
+bd_status bd_profile_enable(bd_ctx* c, int enable) {
+  if (!c) return BD_EINVAL;
+  c->profile = enable != 0;
+  std::fill(c->prof_ms, c->prof_ms + 8, 0.0);
+  std::fill(c->prof_launch, c->prof_launch + 8, 0);
+  return BD_OK;
+}
+
+bd_status bd_profile_read(bd_ctx* c, double* times_ms, int64_t* launches, int cap) {
+  if (!c) return BD_EINVAL;
+  prof_collect(c);
+  for (int i = 0; i < std::min(cap, 8); ++i) {
+    if (times_ms) times_ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_launch[i];
+  }
+  return BD_OK;
+}
+
+// ---- CSR ------------------------------------------------------------------
+bd_status bd_csr_create(bd_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
+                        const int64_t* indptr, const int32_t* indices, const double* values,
+                        bd_csr** out) {
+  if (!ctx || !out || nrows < 0 || ncols < 0 || nnz < 0 || !indptr)
+    return fail(ctx, BD_EINVAL, "bd_csr_create: bad arguments");
+  if (nnz >= (int64_t)INT32_MAX || nrows >= (int64_t)INT32_MAX)
+    return fail(ctx, BD_EINVAL, "bd_csr_create: matrix too large for int32 indexing");
+  if (indptr[0] != 0 || indptr[nrows] != nnz)
+    return fail(ctx, BD_EINVAL, "bd_csr_create: inconsistent indptr");
+  bd_csr* a = new bd_csr();
+  a->ctx = ctx;
+  a->nrows = nrows;
+  a->ncols = ncols;
+  a->nnz = nnz;
+  a->G = pick_g(nrows ? (double)nnz / nrows : 1.0);
+  std::vector<int> rp(nrows + 1);
+  for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)indptr[i];
+  if (dalloc(&a->rowptr, nrows + 1) || dalloc(&a->col, nnz) || dalloc(&a->val, nnz) ||
+      cudaMemcpy(a->rowptr, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice) ||
+      (nnz && cudaMemcpy(a->col, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice)) ||
+      (nnz && cudaMemcpy(a->val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice))) {
+    bd_csr_destroy(a);
+    return fail(ctx, BD_ECUDA, "bd_csr_create: device allocation/copy failed");
+  }
+  *out = a;
+  return BD_OK;
+}
+
+bd_status bd_csr_destroy(bd_csr* a) {
+  if (!a) return BD_OK;
+  cudaFree(a->rowptr);
+  cudaFree(a->col);
+  cudaFree(a->val);
+  delete a;
+  return BD_OK;
+}
+
+bd_status bd_spmv(bd_csr* a, const double* x, double* y, double alpha, double beta) {
+  if (!a) return BD_EINVAL;
+  bd_ctx* ctx = a->ctx;
+  Scope sc(ctx);
+  const int grid = grid_for(ctx, a->nrows, dev::TPB / a->G);
+  switch (a->G) {
+    case 4: dev::k_spmv<4><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
+    case 8: dev::k_spmv<8><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
+    case 16: dev::k_spmv<16><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
+    default: dev::k_spmv<32><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta);
+  }
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// ---- vector utilities -------------------------------------------------------
+static bd_status util_reduce(bd_ctx* ctx, int64_t n, const double* x, const double* y, int fin,
+                             int64_t nmean, double* out) {
+  Scope sc(ctx);
+  TRY(launch_dot(ctx, x, y, n, ctx->util, dev::C_DOT, fin, dev::S_TMP0, -1, nmean));
+  CK(ctx, cudaMemcpyAsync(ctx->h_pin, ctx->util.sc + dev::S_TMP0, sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  *out = ctx->h_pin[0];
+  return BD_OK;
+}
+
+bd_status bd_dot(bd_ctx* ctx, int64_t n, const double* x, const double* y, double* out) {
+  if (!ctx || !out || n < 0) return BD_EINVAL;
+  if (n == 0) {
+    *out = 0.0;
+    return BD_OK;
+  }
+  return util_reduce(ctx, n, x, y, dev::FIN_STORE0, 1, out);
+}
+
+bd_status bd_mean(bd_ctx* ctx, int64_t n, const double* x, double* out) {
+  if (!ctx || !out || n <= 0) return fail(ctx, BD_EINVAL, "bd_mean: empty vector");
+  return util_reduce(ctx, n, x, nullptr, dev::FIN_MEAN, n, out);
+}
+
+// ---- system ---------------------------------------------------------------------
+bd_status bd_system_create(bd_ctx* ctx, bd_csr* S1, bd_csr* Si, const double* mass,
+                           const double* heart_mass, double gamma, bd_system** out) {
+  if (!ctx || !S1 || !Si || !mass || !heart_mass || !out)
+    return fail(ctx, BD_EINVAL, "bd_system_create: null argument");
+  if (S1->nrows != S1->ncols || Si->nrows != Si->ncols || Si->nrows > S1->nrows)
+    return fail(ctx, BD_EINVAL, "bd_system_create: block shapes do not match");
+  bd_system* s = new bd_system();
+  s->ctx = ctx;
+  s->S1 = S1;
+  s->Si = Si;
+  s->n = S1->nrows;
+  s->m = Si->nrows;
+  s->gamma = gamma;
+  if (dalloc(&s->mass, s->n) || dalloc(&s->mh, s->m) || dalloc(&s->tmp, s->n + s->m) ||
+      cudaMemcpy(s->mass, mass, sizeof(double) * s->n, cudaMemcpyHostToDevice) ||
+      cudaMemcpy(s->mh, heart_mass, sizeof(double) * s->m, cudaMemcpyHostToDevice) ||
+      ctl_alloc(&s->ctl, (int64_t)ctx->nsm * 8, 0, 0)) {
+    bd_system_destroy(s);
+    return fail(ctx, BD_ECUDA, "bd_system_create: device allocation failed");
+  }
+  CK(ctx, cudaDeviceSynchronize());
+  // ΣM once, fixed order (bd/system.py:145 denominator)
+  {
+    Scope sc(ctx);
+    bd_status st = launch_dot(ctx, s->mass, nullptr, s->n, s->ctl, dev::C_DOT, dev::FIN_STORE0,
+                              dev::S_MSUM, -1, 1);
+    if (st != BD_OK) return st;
+  }
+  *out = s;
+  return BD_OK;
+}
+
+bd_status bd_system_destroy(bd_system* s) {
+  if (!s) return BD_OK;
+  cudaStreamSynchronize(s->ctx->stream);
+  cudaFree(s->mass);
+  cudaFree(s->mh);
+  cudaFree(s->tmp);
+  ctl_free(&s->ctl);
+  delete s;
+  return BD_OK;
+}
+
+bd_status bd_system_apply(bd_system* s, const double* x, double* q) {
+  if (!s || !x || !q) return BD_EINVAL;
+  Scope sc(s->ctx);
+  return launch_lambda(s, x, q, s->ctl, 0);
+}
+
+bd_status bd_system_normalize(bd_system* s, const double* x, double* y) {
+  if (!s || !x || !y) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  TRY(launch_dot(ctx, s->mass, x, s->n, s->ctl, dev::C_WMEAN, dev::FIN_WMEAN, 0, -1, 1));
+  dev::k_normalize<<<grid_for(ctx, s->n + s->m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      x, y, s->n, s->n + s->m, s->ctl.sc, nullptr);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_system_weighted_mean_u(bd_system* s, const double* u, double* out) {
+  if (!s || !u || !out) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  TRY(launch_dot(ctx, s->mass, u, s->n, s->ctl, dev::C_WMEAN, dev::FIN_WMEAN, 0, -1, 1));
+  CK(ctx, cudaMemcpyAsync(ctx->h_pin, s->ctl.sc + dev::S_WMEAN, sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  *out = ctx->h_pin[0];
+  return BD_OK;
+}
+
+// ---- inner ------------------------------------------------------------------------
+bd_status bd_inner_create(bd_ctx* ctx, int kind, int64_t n, const int64_t* indptr,
+                          const int32_t* indices, const double* values, int max_restarts,
+                          bd_inner** out, int* restarts_used) {
+  if (!ctx || !out || n <= 0 || !indptr) return fail(ctx, BD_EINVAL, "bd_inner_create: bad arguments");
+  if (kind != BD_INNER_EXACT && kind != BD_INNER_IC0 && kind != BD_INNER_JACOBI)
+    return fail(ctx, BD_EINVAL, "unknown inner preconditioner kind");
+  HostCsr a;
+  a.n = n;
+  a.indptr.assign(indptr, indptr + n + 1);
+  a.indices.assign(indices, indices + indptr[n]);
+  a.values.assign(values, values + indptr[n]);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
+      if (a.indices[p] < 0 || a.indices[p] >= n)
+        return fail(ctx, BD_EINVAL, "bd_inner_create: column index out of range");
+      if (p > a.indptr[i] && a.indices[p] <= a.indices[p - 1])
+        return fail(ctx, BD_EINVAL, "bd_inner_create: CSR must be canonical (sorted, no duplicates)");
+    }
+  bd_inner* p = new bd_inner();
+  p->ctx = ctx;
+  p->kind = kind;
+  p->n = n;
+  if (ctl_alloc(&p->ctl, (int64_t)ctx->nsm * 8, 0, 0)) {
+    delete p;
+    return fail(ctx, BD_ECUDA, "bd_inner_create: allocation failed");
+  }
+  if (kind == BD_INNER_JACOBI) {
+    // 1/diag, strictly positive diagonal required (bd/precond.py:224-232)
+    std::vector<double> inv(n);
+    for (int64_t i = 0; i < n; ++i) {
+      double d = 0.0;
+      for (int64_t q = a.indptr[i]; q < a.indptr[i + 1]; ++q)
+        if (a.indices[q] == i) d = a.values[q];
+      if (!(d > 0.0)) {
+        bd_inner_destroy(p);
+        return fail(ctx, BD_EPRECOND, "Jacobi requires a strictly positive diagonal");
+      }
+      inv[i] = 1.0 / d;
+    }
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < n; ++i) nnz += a.indptr[i + 1] - a.indptr[i];
+    p->G = pick_g(n ? (double)nnz / n : 1.0);
+    if (dalloc(&p->inv, n) || cudaMemcpy(p->inv, inv.data(), sizeof(double) * n, cudaMemcpyHostToDevice) ||
+        dalloc(&p->x_int, n)) {
+      bd_inner_destroy(p);
+      return fail(ctx, BD_ECUDA, "bd_inner_create: allocation failed");
+    }
+    if (restarts_used) *restarts_used = 0;
+    CK(ctx, cudaDeviceSynchronize());
+    *out = p;
+    return BD_OK;
+  }
+  std::string msg;
+  HostCsr lower;
+  if (kind == BD_INNER_IC0) {
+    const int rc = ic0_factor(a, max_restarts, &lower, &p->restarts, &msg);
+    if (rc != 0) {
+      bd_inner_destroy(p);
+      return fail(ctx, BD_EPRECOND, msg);
+    }
+  } else {
+    nested_dissection(a, &p->hperm);
+    const int rc = cholesky(a, p->hperm, &lower, &msg);
+    if (rc != 0) {
+      bd_inner_destroy(p);
+      return fail(ctx, BD_EPRECOND, "sparse Cholesky failed, matrix not positive definite: " + msg);
+    }
+  }
+  HostCsr upper = transpose(lower);
+  const double avg = lower.n ? (double)lower.nnz() / lower.n : 1.0;
+  p->G = pick_g(avg - 1.0);
+  bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
+  if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
+  if (st != BD_OK) {
+    bd_inner_destroy(p);
+    return st;
+  }
+  if (dalloc(&p->y_int, n) || dalloc(&p->x_int, n) ||
+      cudaMemset(p->y_int, 0xFF, sizeof(double) * n)) {
+    bd_inner_destroy(p);
+    return fail(ctx, BD_ECUDA, "bd_inner_create: allocation failed");
+  }
+  if (!p->hperm.empty()) {
+    if (dalloc(&p->perm, n) ||
+        cudaMemcpy(p->perm, p->hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice)) {
+      bd_inner_destroy(p);
+      return fail(ctx, BD_ECUDA, "bd_inner_create: allocation failed");
+    }
+  }
+  p->hlower = std::move(lower);
+  if (restarts_used) *restarts_used = p->restarts;
+  CK(ctx, cudaDeviceSynchronize());
+  *out = p;
+  return BD_OK;
+}
+
+bd_status bd_inner_destroy(bd_inner* p) {
+  if (!p) return BD_OK;
+  cudaStreamSynchronize(p->ctx->stream);
+  free_tri(&p->L);
+  free_tri(&p->U);
+  cudaFree(p->perm);
+  cudaFree(p->inv);
+  cudaFree(p->y_int);
+  cudaFree(p->x_int);
+  ctl_free(&p->ctl);
+  delete p;
+  return BD_OK;
+}
+
+bd_status bd_inner_apply(bd_inner* p, const double* y, double* z) {
+  if (!p || !y || !z) return BD_EINVAL;
+  Scope sc(p->ctx);
+  dev::RhsVec rhs{y, (int)p->n, nullptr, p->perm};
+  if (p->kind == BD_INNER_JACOBI) return inner_solve(p, rhs, z, nullptr, p->ctl, dev::C_JAC1);
+  return inner_solve(p, rhs, p->x_int, z, p->ctl, dev::C_BULK1_S);
+}
+
+bd_status bd_inner_factor_info(bd_inner* p, int64_t* n, int64_t* nnz, int64_t* levels) {
+  if (!p) return BD_EINVAL;
+  if (n) *n = p->n;
+  if (nnz) *nnz = p->kind == BD_INNER_JACOBI ? p->n : p->hlower.nnz();
+  if (levels) *levels = p->kind == BD_INNER_JACOBI ? 1 : std::max(p->L.depth, p->U.depth);
+  return BD_OK;
+}
+
+bd_status bd_inner_export_factor(bd_inner* p, int64_t* indptr, int32_t* indices, double* values,
+                                 int32_t* perm) {
+  if (!p) return BD_EINVAL;
+  if (p->kind == BD_INNER_JACOBI) return fail(p->ctx, BD_EINVAL, "jacobi has no factor");
+  const HostCsr& l = p->hlower;
+  if (indptr) std::copy(l.indptr.begin(), l.indptr.end(), indptr);
+  if (indices) std::copy(l.indices.begin(), l.indices.end(), indices);
+  if (values) std::copy(l.values.begin(), l.values.end(), values);
+  if (perm) {
+    if (p->hperm.empty())
+      for (int64_t i = 0; i < p->n; ++i) perm[i] = (int32_t)i;
+    else
+      std::copy(p->hperm.begin(), p->hperm.end(), perm);
+  }
+  return BD_OK;
+}
+
+// ---- block-LU ---------------------------------------------------------------------
+bd_status bd_blocklu_create(bd_system* s, bd_inner* bulk, bd_inner* schur, double beta,
+                            bd_prec** out) {
+  if (!s || !bulk || !schur || !out) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  if (bulk->n != s->n || schur->n != s->m)
+    return fail(ctx, BD_EINVAL, "bd_blocklu_create: inner sizes do not match the system");
+  if (!(beta > 0.0)) return fail(ctx, BD_EINVAL, "bd_blocklu_create: beta must be positive");
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  bd_prec* p = new bd_prec();
+  p->sys = s;
+  p->bulk = bulk;
+  p->schur = schur;
+  p->beta = beta;
+  const int64_t n = s->n, m = s->m, nm = n + m;
+  int64_t parts = (int64_t)ctx->nsm * 8 * 2;
+  parts = std::max<int64_t>(parts, std::max(bulk->U.nvb, schur->U.nvb));
+  p->hist_cap = 0;
+  if (ctl_alloc(&p->ctl, parts, 0, 1) || dalloc(&p->traw, n) || dalloc(&p->z2raw, n) ||
+      dalloc(&p->corr, m) || dalloc(&p->sbuf, m) || dalloc(&p->x, nm) || dalloc(&p->r, nm) ||
+      dalloc(&p->z, nm) || dalloc(&p->d, nm) || dalloc(&p->q, nm)) {
+    bd_blocklu_destroy(p);
+    return fail(ctx, BD_ECUDA, "bd_blocklu_create: allocation failed");
+  }
+  p->ctl_nf = p->ctl;
+  p->ctl_nf.use_flags = 0;
+  CK(ctx, cudaDeviceSynchronize());
+  // beta and ΣM into the slots
+  CK(ctx, cudaMemcpy(p->ctl.sc + dev::S_BULK_BETA, &beta, sizeof(double), cudaMemcpyHostToDevice));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemcpy(p->ctl.sc + dev::S_MSUM, s->ctl.sc + dev::S_MSUM, sizeof(double),
+                     cudaMemcpyDeviceToDevice));
+  const char* env = getenv("BD_NO_GRAPH");
+  p->use_graph = !(env && env[0] == '1');
+  *out = p;
+  return BD_OK;
+}
+
+bd_status bd_blocklu_destroy(bd_prec* p) {
+  if (!p) return BD_OK;
+  cudaStreamSynchronize(p->sys->ctx->stream);
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  ctl_free(&p->ctl);
+  cudaFree(p->traw);
+  cudaFree(p->z2raw);
+  cudaFree(p->corr);
+  cudaFree(p->sbuf);
+  cudaFree(p->x);
+  cudaFree(p->r);
+  cudaFree(p->z);
+  cudaFree(p->d);
+  cudaFree(p->q);
+  delete p;
+  return BD_OK;
+}
+
+bd_status bd_blocklu_apply(bd_prec* p, const double* r, double* z) {
+  if (!p || !r || !z) return BD_EINVAL;
+  bd_system* s = p->sys;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  const Ctl& c = p->ctl_nf;
+  TRY(launch_dot(ctx, r, nullptr, s->n, c, dev::C_MEAN, dev::FIN_MEAN, dev::S_MU1, dev::S_C1, s->n));
+  TRY(enqueue_pinv(p, r, z, p->sbuf, z + s->n, c, false));
+  p->cnt[0] += 2;
+  p->cnt[1] += 1;
+  p->cnt[2] += 2;
+  return BD_OK;
+}
+
+bd_status bd_blocklu_bulk_inverse(bd_prec* p, const double* y, double* z) {
+  if (!p || !y || !z) return BD_EINVAL;
+  bd_system* s = p->sys;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  const Ctl& c = p->ctl_nf;
+  const int64_t n = s->n;
+  // mean, inner(y - mean), recentre, + mean/beta  (bd/precond.py:281-292)
+  TRY(launch_dot(ctx, y, nullptr, n, c, dev::C_MEAN, dev::FIN_MEAN, dev::S_MU1, dev::S_C1, n));
+  dev::RhsVec rhs{y, (int)n, c.sc + dev::S_MU1, p->bulk->perm};
+  double* xi = p->bulk->perm ? p->bulk->x_int : p->traw;
+  double* o = p->bulk->perm ? p->traw : nullptr;
+  if (p->bulk->kind == BD_INNER_JACOBI) {
+    xi = p->traw;
+    o = nullptr;
+  }
+  TRY(inner_solve(p->bulk, rhs, xi, o, c, dev::C_BULK1_S, dev::FIN_MEAN, dev::S_MT, -1, n));
+  // z = (traw - mt) + c1: k_combine with a zero second operand
+  CK(ctx, cudaMemsetAsync(c.sc + dev::S_M2, 0, sizeof(double), ctx->stream));
+  CK(ctx, cudaMemsetAsync(c.sc + dev::S_C2, 0, sizeof(double), ctx->stream));
+  CK(ctx, cudaMemsetAsync(p->z2raw, 0, sizeof(double) * n, ctx->stream));
+  dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->traw, p->z2raw, z, n,
+                                                                           c, 0);
+  LAUNCHED(ctx);
+  p->cnt[0] += 1;
+  return BD_OK;
+}
+
+bd_status bd_blocklu_schur_inverse(bd_prec* p, const double* y, double* z) {
+  if (!p || !y || !z) return BD_EINVAL;
+  Scope sc(p->sys->ctx);
+  dev::RhsVec rhs{y, (int)p->sys->m, nullptr, p->schur->perm};
+  bd_status st;
+  if (p->schur->kind == BD_INNER_JACOBI)
+    st = inner_solve(p->schur, rhs, z, nullptr, p->ctl_nf, dev::C_JAC2);
+  else
+    st = inner_solve(p->schur, rhs, p->schur->x_int, z, p->ctl_nf, dev::C_SCH_S);
+  if (st == BD_OK) p->cnt[1] += 1;
+  return st;
+}
+
+bd_status bd_blocklu_counters(bd_prec* p, int64_t* counters) {
+  if (!p || !counters) return BD_EINVAL;
+  std::copy(p->cnt, p->cnt + 3, counters);
+  return BD_OK;
+}
+
+bd_status bd_blocklu_reset_counters(bd_prec* p) {
+  if (!p) return BD_EINVAL;
+  std::fill(p->cnt, p->cnt + 3, 0);
+  return BD_OK;
+}
+
+// ---- PCG ----------------------------------------------------------------------------
+bd_status bd_pcg_solve(bd_system* s, bd_prec* p, const double* b, const double* x0, double tol,
+                       int64_t max_iter, double* x, bd_stats* stats, double* res_hist,
+                       int64_t* n_res, double* prec_hist, int64_t* n_prec) {
+  if (!s || !p || !b || !x || !stats) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  std::memset(stats, 0, sizeof(*stats));
+  stats->curvature = std::nan("");
+  if (!(tol > 0.0)) return fail(ctx, BD_EINVAL, "tol must be strictly positive");
+  if (max_iter < 0) return fail(ctx, BD_EINVAL, "max_iter must be non-negative");
+  if (p->sys != s) return fail(ctx, BD_EINVAL, "preconditioner was built for another system");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = s->n, nm = s->n + s->m;
+  // history buffers (device), regrown on demand (invalidates the graph)
+  const int need = (int)std::min<int64_t>(max_iter + 2, (int64_t)INT32_MAX);
+  if (need > p->hist_cap) {
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(p->ctl.res_hist);
+    cudaFree(p->ctl.prec_hist);
+    const int cap = std::max(need, 512);
+    CK(ctx, dalloc(&p->ctl.res_hist, cap));
+    CK(ctx, dalloc(&p->ctl.prec_hist, cap));
+    p->hist_cap = cap;
+    p->ctl.hist_cap = cap;
+    p->ctl_nf = p->ctl;
+    p->ctl_nf.use_flags = 0;
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      cudaGraphDestroy(p->graph);
+      p->gexec = nullptr;
+      p->graph = nullptr;
+    }
+  }
+  if (p->use_graph && !ctx->profile && !p->gexec) TRY(build_graph(p));
+  Scope scope(ctx);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, ctx->stream);
+  // control block init: flags, tol, max_iter
+  {
+    int* hf = (int*)ctx->h_pin;
+    std::memset(hf, 0, sizeof(int) * dev::NFLAGS);
+    hf[dev::F_FIRST] = 1;
+    hf[dev::F_MAXITER] = (int)std::min<int64_t>(max_iter, INT32_MAX);
+    CK(ctx, cudaMemcpyAsync(p->ctl.fl, hf, sizeof(int) * dev::NFLAGS, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    double* hs = ctx->h_pin + 16;
+    hs[0] = tol;
+    CK(ctx, cudaMemcpyAsync(p->ctl.sc + dev::S_TOL, hs, sizeof(double), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    // the pinned staging area is reused below only after a synchronise
+  }
+  const Ctl& c = p->ctl;
+  prof_mark(ctx, 6);
+  // ||b|| (and the zero-rhs exit)
+  TRY(launch_dot(ctx, b, b, nm, c, dev::C_NORMB, dev::FIN_RHSNORM, 0, -1, 1));
+  // x0 / r0
+  if (x0) {
+    dev::k_copy<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->x, x0, nm, c);
+    LAUNCHED(ctx);
+    TRY(launch_lambda(s, p->x, p->q, c, 0));
+    dev::k_init_res<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(b, p->q, p->r, n,
+                                                                               nm, c);
+  } else {
+    dev::k_fill<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->x, nm, 0LL, c);
+    LAUNCHED(ctx);
+    dev::k_init_res<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(b, nullptr, p->r, n,
+                                                                               nm, c);
+  }
+  LAUNCHED(ctx);
+  dev::k_fill<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->d, nm, 0LL, c);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 1);
+  // z0 = deflate(P^{-1} r0); rho0; d0 = z0
+  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));
+  dev::k_rho<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->r, p->z, n, nm, c);
+  LAUNCHED(ctx);
+  dev::k_dupdate<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->z, p->d, n, nm, c);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 5);
+  int* hflag = (int*)(ctx->h_pin + 32);
+  int64_t it_launch = 0;
+  if (p->gexec && !ctx->profile) {
+    CK(ctx, cudaGraphLaunch(p->gexec, ctx->stream));
+    ctx->launches += 1;
+    it_launch = -1;  // counted from the iteration count below
+  } else {
+    int batch = 2;
+    for (;;) {
+      for (int i = 0; i < batch; ++i) TRY(enqueue_iteration(p));
+      CK(ctx, cudaMemcpyAsync(hflag, c.fl, sizeof(int) * dev::NFLAGS, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      CK(ctx, cudaStreamSynchronize(ctx->stream));
+      if (hflag[dev::F_DONE] || hflag[dev::F_STOP]) break;
+      batch = std::min(batch * 2, 32);
+    }
+  }
+  // x <- normalize(x) (bd/system.py:138-146), zero for a zero rhs
+  TRY(launch_dot(ctx, s->mass, p->x, n, p->ctl_nf, dev::C_WMEAN, dev::FIN_WMEAN, 0, -1, 1));
+  dev::k_normalize<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->x, x, n, nm,
+                                                                             c.sc, c.fl);
+  LAUNCHED(ctx);
+  prof_mark(ctx, 5);
+  cudaEventRecord(e1, ctx->stream);
+  // readback
+  CK(ctx, cudaMemcpyAsync(hflag, c.fl, sizeof(int) * dev::NFLAGS, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  double* hsc = ctx->h_pin;
+  CK(ctx, cudaMemcpyAsync(hsc, c.sc, sizeof(double) * 24, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  const int nres = std::min(hflag[dev::F_NRES], p->hist_cap);
+  const int nprec = std::min(hflag[dev::F_NPREC], p->hist_cap);
+  if (res_hist && nres)
+    CK(ctx, cudaMemcpy(res_hist, c.res_hist, sizeof(double) * nres, cudaMemcpyDeviceToHost));
+  if (prec_hist && nprec)
+    CK(ctx, cudaMemcpy(prec_hist, c.prec_hist, sizeof(double) * nprec, cudaMemcpyDeviceToHost));
+  if (n_res) *n_res = nres;
+  if (n_prec) *n_prec = nprec;
+  float dms = 0.f;
+  cudaEventElapsedTime(&dms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  prof_collect(ctx);
+  stats->iterations = hflag[dev::F_ITERS];
+  stats->mv_count = hflag[dev::F_NMV];
+  stats->p1_count = 2 * (int64_t)hflag[dev::F_NAPP];
+  stats->pk_count = hflag[dev::F_NAPP];
+  stats->converged = hflag[dev::F_CONV];
+  stats->device_ms = dms;
+  stats->final_residual = 0.0;
+  if (nres)
+    CK(ctx, cudaMemcpy(&stats->final_residual, c.res_hist + (nres - 1), sizeof(double),
+                       cudaMemcpyDeviceToHost));
+  p->cnt[0] += stats->p1_count;
+  p->cnt[1] += stats->pk_count;
+  p->cnt[2] += 2 * (int64_t)hflag[dev::F_NAPP];
+  if (it_launch < 0)  // graph bodies run once per iteration (+1 for the exit test)
+    ctx->launches += (iteration_launches(p) + 1) * (int64_t)std::max<int64_t>(stats->iterations, 1);
+  bd_status st = BD_OK;
+  if (hflag[dev::F_STATUS] == dev::ST_EBREAKDOWN) {
+    st = BD_EBREAKDOWN;
+    stats->curvature = hsc[dev::S_CURV];
+    char buf[128];
+    if (std::isnan(hsc[dev::S_CURV]) && stats->iterations > 0 && hsc[dev::S_DQ] > 0)
+      std::snprintf(buf, sizeof buf, "non-finite residual");
+    else
+      std::snprintf(buf, sizeof buf, "conjugate gradient breakdown: curvature %g", hsc[dev::S_CURV]);
+    ctx->err = buf;
+  } else if (!hflag[dev::F_CONV]) {
+    st = BD_ENOCONV;
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "PCG did not reach tol=%g within %lld iterations (residual %.3e)",
+                  tol, (long long)max_iter, stats->final_residual);
+    ctx->err = buf;
+  }
+  stats->status = st;
+  stats->wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return st;
+}
+
+// ---- membrane -------------------------------------------------------------------
+bd_status bd_membrane_rhs(bd_system* s, const double* v, const double* w, const uint64_t* site_mask,
+                          uint64_t active_sites, double amplitude, double chi, double v_rest,
+                          double v_span, double tau_in, double tau_out, double c_m, double* rhs,
+                          double* ion) {
+  if (!s || !v || !w || !rhs) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  dev::k_membrane_rhs<<<grid_for(ctx, s->n + s->m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      s->n, s->m, v, w, site_mask, active_sites, amplitude, chi, s->gamma, s->mh, v_rest, v_span,
+      tau_in, tau_out, c_m, rhs, ion);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double* w, double dt,
+                           double v_rest, double v_span, double tau_open, double tau_close,
+                           double u_gate, double* w_new) {
+  if (!ctx || !v || !w || !w_new) return BD_EINVAL;
+  if (!(dt > 0.0)) return fail(ctx, BD_EINVAL, "dt must be strictly positive");
+  Scope sc(ctx);
+  dev::k_membrane_gate<<<grid_for(ctx, m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      m, v, w, dt, v_rest, v_span, tau_open, tau_close, u_gate, w_new);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+}  // extern "C"

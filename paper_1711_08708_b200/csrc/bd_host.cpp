@@ -1,0 +1,458 @@
+// Host-side setup of the inner preconditioners (compiled with
+// -ffp-contract=off so the IC(0) sweep rounds exactly like the numpy scalar
+// arithmetic of the reference).
+#include "bd_host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+
+namespace bd {
+
+namespace {
+
+// Sorted-merge dot product of two sparse row prefixes
+// (_sparse_row_dot, bd/precond.py:201-216): products accumulated left to
+// right in ascending column order, starting from 0.0.
+double merge_dot(const int32_t* ca, const double* va, int64_t na, const int32_t* cb,
+                 const double* vb, int64_t nb) {
+  int64_t ia = 0, ib = 0;
+  double out = 0.0;
+  while (ia < na && ib < nb) {
+    const int32_t a = ca[ia], b = cb[ib];
+    if (a == b) {
+      const double prod = va[ia] * vb[ib];
+      out = out + prod;
+      ++ia;
+      ++ib;
+    } else if (a < b) {
+      ++ia;
+    } else {
+      ++ib;
+    }
+  }
+  return out;
+}
+
+// One factorisation sweep over tril(A) (bd/precond.py:170-189); false on a
+// non-positive pivot.  `val` holds the (possibly diagonal-scaled) copy.
+bool ic0_sweep(const HostCsr& t, std::vector<double>& val) {
+  const int64_t* ip = t.indptr.data();
+  const int32_t* ci = t.indices.data();
+  double* v = val.data();
+  for (int64_t i = 0; i < t.n; ++i) {
+    const int64_t rs = ip[i], re = ip[i + 1];
+    for (int64_t idx = rs; idx < re; ++idx) {
+      const int32_t j = ci[idx];
+      const int64_t js = ip[j], je = ip[j + 1];
+      const double s = merge_dot(ci + rs, v + rs, idx - rs, ci + js, v + js, (je - 1) - js);
+      if (j == i) {
+        const double pivot = v[idx] - s;
+        if (pivot <= 0.0) return false;
+        v[idx] = std::sqrt(pivot);
+      } else {
+        v[idx] = (v[idx] - s) / v[ip[j + 1] - 1];
+      }
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+int ic0_factor(const HostCsr& a, int max_restarts, HostCsr* lower, int* restarts_used,
+               std::string* msg) {
+  // lower = tril(a) keeping stored entries (bd/precond.py:158)
+  HostCsr t;
+  t.n = a.n;
+  t.indptr.assign(a.n + 1, 0);
+  for (int64_t i = 0; i < a.n; ++i) {
+    int64_t c = 0;
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p)
+      if (a.indices[p] <= i) ++c;
+    t.indptr[i + 1] = t.indptr[i] + c;
+  }
+  t.indices.resize(t.indptr[a.n]);
+  t.values.resize(t.indptr[a.n]);
+  for (int64_t i = 0; i < a.n; ++i) {
+    int64_t o = t.indptr[i];
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p)
+      if (a.indices[p] <= i) {
+        t.indices[o] = a.indices[p];
+        t.values[o] = a.values[p];
+        ++o;
+      }
+  }
+  // diagonal must be the last stored entry of every row (:160-166)
+  std::vector<int64_t> diag_pos(a.n);
+  for (int64_t i = 0; i < a.n; ++i) {
+    const int64_t last = t.indptr[i + 1] - 1;
+    if (last < t.indptr[i] || t.indices[last] != i) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "missing diagonal entry in row %lld", (long long)i);
+      *msg = buf;
+      return 1;
+    }
+    diag_pos[i] = last;
+  }
+  double shift = 1.0;
+  for (int attempt = 0; attempt <= max_restarts; ++attempt) {
+    std::vector<double> val = t.values;
+    if (shift != 1.0)
+      for (int64_t i = 0; i < a.n; ++i) val[diag_pos[i]] = val[diag_pos[i]] * shift;
+    if (ic0_sweep(t, val)) {
+      lower->n = t.n;
+      lower->indptr = t.indptr;
+      lower->indices = t.indices;
+      lower->values = std::move(val);
+      if (restarts_used) *restarts_used = attempt;
+      return 0;
+    }
+    shift = shift * (1.0 + 1e-3);
+  }
+  char buf[128];
+  std::snprintf(buf, sizeof buf,
+                "incomplete Cholesky failed after %d diagonal shift restarts", max_restarts);
+  *msg = buf;
+  return 2;
+}
+
+HostCsr transpose(const HostCsr& a) {
+  HostCsr t;
+  // square factors only on this path
+  t.n = a.n;
+  t.indptr.assign(a.n + 1, 0);
+  const int64_t nnz = a.nnz();
+  for (int64_t p = 0; p < nnz; ++p) t.indptr[a.indices[p] + 1]++;
+  for (int64_t i = 0; i < a.n; ++i) t.indptr[i + 1] += t.indptr[i];
+  t.indices.resize(nnz);
+  t.values.resize(nnz);
+  std::vector<int64_t> next(t.indptr.begin(), t.indptr.end() - 1);
+  for (int64_t i = 0; i < a.n; ++i)
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
+      const int64_t o = next[a.indices[p]]++;
+      t.indices[o] = (int32_t)i;
+      t.values[o] = a.values[p];
+    }
+  return t;
+}
+
+int64_t row_levels(const HostCsr& t, bool lower, std::vector<int32_t>* level) {
+  level->assign(t.n, 0);
+  int32_t depth = 0;
+  auto visit = [&](int64_t i) {
+    int32_t lv = 0;
+    for (int64_t p = t.indptr[i]; p < t.indptr[i + 1]; ++p) {
+      const int32_t j = t.indices[p];
+      if (j != i) lv = std::max(lv, (*level)[j] + 1);
+    }
+    (*level)[i] = lv;
+    depth = std::max(depth, lv + 1);
+  };
+  if (lower)
+    for (int64_t i = 0; i < t.n; ++i) visit(i);
+  else
+    for (int64_t i = t.n - 1; i >= 0; --i) visit(i);
+  return depth;
+}
+
+void build_schedule(const std::vector<int32_t>& level, int64_t depth, int pad,
+                    std::vector<int32_t>* tasks) {
+  std::vector<int64_t> count(depth + 1, 0);
+  for (int32_t lv : level) count[lv + 1]++;
+  std::vector<int64_t> start(depth + 1, 0);  // padded offsets
+  for (int64_t l = 0; l < depth; ++l) {
+    const int64_t c = count[l + 1];
+    start[l + 1] = start[l] + (c + pad - 1) / pad * pad;
+  }
+  tasks->assign(start[depth], -1);
+  std::vector<int64_t> fill(start.begin(), start.end() - 1);
+  for (int64_t i = 0; i < (int64_t)level.size(); ++i) (*tasks)[fill[level[i]]++] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// Nested dissection on the symmetric pattern.
+namespace {
+
+struct Graph {
+  int64_t n;
+  std::vector<int64_t> xadj;
+  std::vector<int32_t> adj;
+};
+
+Graph symmetric_graph(const HostCsr& a) {
+  // pattern of A + A^T without the diagonal
+  std::vector<int64_t> deg(a.n, 0);
+  for (int64_t i = 0; i < a.n; ++i)
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
+      const int32_t j = a.indices[p];
+      if (j == i) continue;
+      deg[i]++;
+      deg[j]++;
+    }
+  Graph g;
+  g.n = a.n;
+  g.xadj.assign(a.n + 1, 0);
+  for (int64_t i = 0; i < a.n; ++i) g.xadj[i + 1] = g.xadj[i] + deg[i];
+  g.adj.resize(g.xadj[a.n]);
+  std::vector<int64_t> pos(g.xadj.begin(), g.xadj.end() - 1);
+  for (int64_t i = 0; i < a.n; ++i)
+    for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
+      const int32_t j = a.indices[p];
+      if (j == i) continue;
+      g.adj[pos[i]++] = j;
+      g.adj[pos[j]++] = (int32_t)i;
+    }
+  // dedupe each adjacency list
+  std::vector<int64_t> nx(a.n + 1, 0);
+  int64_t w = 0;
+  for (int64_t i = 0; i < a.n; ++i) {
+    auto b = g.adj.begin() + g.xadj[i], e = g.adj.begin() + g.xadj[i + 1];
+    std::sort(b, e);
+    auto u = std::unique(b, e);
+    const int64_t len = u - b;
+    std::copy(b, u, g.adj.begin() + w);
+    nx[i] = w;
+    w += len;
+  }
+  nx[a.n] = w;
+  g.adj.resize(w);
+  g.xadj = std::move(nx);
+  return g;
+}
+
+struct NdState {
+  const Graph* g;
+  std::vector<int32_t> part;   // subset id of each node
+  std::vector<int32_t> dist;   // BFS scratch
+  std::vector<int32_t>* out;
+  int32_t next_id = 1;
+};
+
+// BFS inside subset `id` from `root`; fills order (visited nodes) and dist.
+void bfs(NdState& st, int32_t id, int32_t root, std::vector<int32_t>& order) {
+  order.clear();
+  order.push_back(root);
+  st.dist[root] = 0;
+  for (size_t h = 0; h < order.size(); ++h) {
+    const int32_t u = order[h];
+    for (int64_t p = st.g->xadj[u]; p < st.g->xadj[u + 1]; ++p) {
+      const int32_t v = st.g->adj[p];
+      if (st.part[v] == id && st.dist[v] < 0) {
+        st.dist[v] = st.dist[u] + 1;
+        order.push_back(v);
+      }
+    }
+  }
+}
+
+void reset_dist(NdState& st, const std::vector<int32_t>& nodes) {
+  for (int32_t u : nodes) st.dist[u] = -1;
+}
+
+void dissect(NdState& st, std::vector<int32_t> nodes, int32_t id) {
+  const size_t kLeaf = 48;
+  if (nodes.size() <= kLeaf) {
+    std::sort(nodes.begin(), nodes.end());
+    for (int32_t u : nodes) st.out->push_back(u);
+    return;
+  }
+  // pseudo-peripheral root: repeated BFS to a farthest node
+  std::vector<int32_t> order;
+  int32_t root = *std::min_element(nodes.begin(), nodes.end());
+  int32_t ecc = -1;
+  for (int rep = 0; rep < 4; ++rep) {
+    bfs(st, id, root, order);
+    const int32_t far = order.back();
+    const int32_t e = st.dist[far];
+    reset_dist(st, order);
+    if (e <= ecc) break;
+    ecc = e;
+    root = far;
+  }
+  bfs(st, id, root, order);
+  if (order.size() < nodes.size()) {
+    // disconnected: split off this component, recurse on both
+    std::vector<int32_t> comp(order), rest;
+    reset_dist(st, order);
+    const int32_t id_c = st.next_id++, id_r = st.next_id++;
+    for (int32_t u : comp) st.part[u] = id_c;
+    for (int32_t u : nodes)
+      if (st.part[u] == id) {
+        st.part[u] = id_r;
+        rest.push_back(u);
+      }
+    dissect(st, std::move(comp), id_c);
+    dissect(st, std::move(rest), id_r);
+    return;
+  }
+  const int32_t maxd = st.dist[order.back()];
+  if (maxd < 2) {  // (near-)clique: no useful separator
+    reset_dist(st, order);
+    std::sort(nodes.begin(), nodes.end());
+    for (int32_t u : nodes) st.out->push_back(u);
+    return;
+  }
+  // level sizes; separator = the smallest level among those near the median
+  std::vector<int64_t> lsize(maxd + 1, 0);
+  for (int32_t u : order) lsize[st.dist[u]]++;
+  int64_t acc = 0;
+  int32_t mid = 1;
+  for (int32_t l = 0; l <= maxd; ++l) {
+    acc += lsize[l];
+    if (2 * acc >= (int64_t)nodes.size()) {
+      mid = l;
+      break;
+    }
+  }
+  mid = std::min(std::max(mid, 1), maxd - 1);
+  int32_t best = mid;
+  const int32_t span = std::max<int32_t>(1, maxd / 8);
+  for (int32_t l = std::max(1, mid - span); l <= std::min(maxd - 1, mid + span); ++l)
+    if (lsize[l] < lsize[best]) best = l;
+  std::vector<int32_t> a, b, s;
+  for (int32_t u : order) {
+    const int32_t d = st.dist[u];
+    if (d < best) a.push_back(u);
+    else if (d > best) b.push_back(u);
+    else s.push_back(u);
+  }
+  reset_dist(st, order);
+  const int32_t ia = st.next_id++, ib = st.next_id++, is = st.next_id++;
+  for (int32_t u : a) st.part[u] = ia;
+  for (int32_t u : b) st.part[u] = ib;
+  for (int32_t u : s) st.part[u] = is;
+  dissect(st, std::move(a), ia);
+  dissect(st, std::move(b), ib);
+  std::sort(s.begin(), s.end());
+  for (int32_t u : s) st.out->push_back(u);
+}
+
+}  // namespace
+
+void nested_dissection(const HostCsr& a, std::vector<int32_t>* perm) {
+  Graph g = symmetric_graph(a);
+  NdState st;
+  st.g = &g;
+  st.part.assign(a.n, 0);
+  st.dist.assign(a.n, -1);
+  perm->clear();
+  perm->reserve(a.n);
+  st.out = perm;
+  std::vector<int32_t> all(a.n);
+  std::iota(all.begin(), all.end(), 0);
+  dissect(st, std::move(all), 0);
+}
+
+// ---------------------------------------------------------------------------
+// Up-looking sparse Cholesky of C = P A P^T.
+int cholesky(const HostCsr& a, const std::vector<int32_t>& perm, HostCsr* lower,
+             std::string* msg) {
+  const int64_t n = a.n;
+  std::vector<int32_t> inv(n);
+  for (int64_t k = 0; k < n; ++k) inv[perm[k]] = (int32_t)k;
+  // C rows, lower part (cols <= row) sorted
+  std::vector<int64_t> cp(n + 1, 0);
+  for (int64_t k = 0; k < n; ++k) {
+    const int32_t r = perm[k];
+    int64_t c = 0;
+    for (int64_t p = a.indptr[r]; p < a.indptr[r + 1]; ++p)
+      if (inv[a.indices[p]] <= k) ++c;
+    cp[k + 1] = cp[k] + c;
+  }
+  std::vector<int32_t> ci(cp[n]);
+  std::vector<double> cx(cp[n]);
+  for (int64_t k = 0; k < n; ++k) {
+    const int32_t r = perm[k];
+    int64_t o = cp[k];
+    for (int64_t p = a.indptr[r]; p < a.indptr[r + 1]; ++p) {
+      const int32_t j = inv[a.indices[p]];
+      if (j <= k) {
+        ci[o] = j;
+        cx[o] = a.values[p];
+        ++o;
+      }
+    }
+  }
+  // elimination tree
+  std::vector<int32_t> parent(n, -1), anc(n, -1);
+  for (int64_t k = 0; k < n; ++k) {
+    for (int64_t p = cp[k]; p < cp[k + 1]; ++p) {
+      int32_t i = ci[p];
+      while (i != -1 && i < k) {
+        const int32_t nx = anc[i];
+        anc[i] = (int32_t)k;
+        if (nx == -1) parent[i] = (int32_t)k;
+        i = nx;
+      }
+    }
+  }
+  // row patterns via ereach; first pass counts columns
+  std::vector<int32_t> s(n), mark(n, -1);
+  auto ereach = [&](int64_t k) -> int64_t {
+    int64_t top = n;
+    mark[k] = (int32_t)k;
+    for (int64_t p = cp[k]; p < cp[k + 1]; ++p) {
+      int32_t i = ci[p];
+      if (i >= k) continue;
+      int64_t len = 0;
+      for (; mark[i] != k; i = parent[i]) {
+        s[len++] = i;
+        mark[i] = (int32_t)k;
+      }
+      while (len > 0) s[--top] = s[--len];
+    }
+    return top;
+  };
+  std::vector<int64_t> colcount(n, 1);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t top = ereach(k);
+    for (int64_t p = top; p < n; ++p) colcount[s[p]]++;
+  }
+  std::fill(mark.begin(), mark.end(), -1);
+  // CSC of L, diagonal first in each column
+  std::vector<int64_t> lp(n + 1, 0);
+  for (int64_t j = 0; j < n; ++j) lp[j + 1] = lp[j] + colcount[j];
+  std::vector<int32_t> li(lp[n]);
+  std::vector<double> lx(lp[n]);
+  std::vector<int64_t> c(lp.begin(), lp.end() - 1);
+  std::vector<double> x(n, 0.0);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t top = ereach(k);
+    double d = 0.0;
+    for (int64_t p = cp[k]; p < cp[k + 1]; ++p) {
+      if (ci[p] == k) d += cx[p];
+      else x[ci[p]] += cx[p];
+    }
+    for (int64_t p = top; p < n; ++p) {
+      const int32_t i = s[p];
+      const double lki = x[i] / lx[lp[i]];
+      x[i] = 0.0;
+      for (int64_t q = lp[i] + 1; q < c[i]; ++q) x[li[q]] -= lx[q] * lki;
+      d -= lki * lki;
+      const int64_t o = c[i]++;
+      li[o] = (int32_t)k;
+      lx[o] = lki;
+    }
+    if (!(d > 0.0)) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "non-positive pivot %g at row %lld", d, (long long)k);
+      *msg = buf;
+      return 2;
+    }
+    const int64_t o = c[k]++;
+    li[o] = (int32_t)k;
+    lx[o] = std::sqrt(d);
+  }
+  // CSC(L) read as CSR is L^T; transpose gives CSR(L) with the diagonal last.
+  HostCsr lt;
+  lt.n = n;
+  lt.indptr = std::move(lp);
+  lt.indices = std::move(li);
+  lt.values = std::move(lx);
+  *lower = transpose(lt);
+  return 0;
+}
+
+}  // namespace bd
