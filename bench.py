@@ -1,0 +1,454 @@
+"""Benchmark: bidomain PCG time-steps/s on B200 (BASELINE.json metric).
+
+Workload (N=1): config 2 — the 128×128×64 Kuhn-split orthotropic slab
+(1,081,665 vertices, 2,163,330 fp64 unknowns), fibres rotating 120° through
+the wall, Mitchell–Schaeffer membrane, corner stimulus, dt 0.05 ms, PCG tol
+1e-10, block-LU/monodomain preconditioner with IC(0) inners.  A "step" is one
+full semi-implicit time step (membrane RHS → warm-started PCG → gate), the
+time loop's unit (bd/simulate.py:134-170).  Inputs are larger than L2
+(≈1.9 GB streamed per PCG iteration vs 126 MB L2), so no explicit flush.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                  [--workload cfg0|cfg1|cfg2|cfg3] [--inner ic0|exact|jacobi]
+
+N>1 (torchrun): one process per GPU; round 1 runs independent replicas of
+the workload per GPU (weak scaling, no data-path collective).
+`--impl reference` times the CPU oracle port (the reference algorithm in
+numpy/scipy, oracle/) on this host, each step a bounded sample of PCG
+iterations extrapolated with the oracle's own iterations per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "bidomain PCG time-steps/s"
+UNIT = "steps/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak_hbm():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(name, inner, cells=None):
+    from paper_1711_08708_b200 import configs
+    builder = configs.BUILDERS[name]
+    wl = builder(cells) if cells is not None else builder()
+    if inner:
+        wl.inner = inner
+    return wl
+
+
+def assemble(wl):
+    from paper_1711_08708_b200.precond import build_monodomain_matrix
+    from paper_1711_08708_b200.system import BidomainSystem
+    t0 = time.perf_counter()
+    sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
+    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+    return sysm, km, time.perf_counter() - t0
+
+
+def tri_bytes(nnz, rows):
+    """Algorithmic bytes of one triangular pass."""
+    return 12 * nnz + 4 * (rows + 1) + 16 * rows
+
+
+def iteration_bytes(n, m, nnz_s1, nnz_si, nnz_l1, nnz_lk):
+    """B_iter of SURVEY §8d (ic0 inners)."""
+    return (12 * nnz_s1 + 36 * nnz_si + 48 * nnz_l1 + 24 * nnz_lk + 20 * (n + m) + 40
+            + 8 * (26 * n + 23 * m))
+
+
+# ---------------------------------------------------------------------------------
+def run_native(args, rank, world, local_rank):
+    import torch
+    import paper_1711_08708_b200 as bd
+    from paper_1711_08708_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = _lib.Context(local_rank)
+    _lib.Context._default = ctx
+
+    wl = build_workload(args.workload, args.inner)
+    sysm, km, t_asm = assemble(wl)
+    t0 = time.perf_counter()
+    pre = bd.BlockLUPreconditioner(sysm, inner=wl.inner, monodomain_matrix=km)
+    t_setup = time.perf_counter() - t0
+    n, m = sysm.n, sysm.n_heart
+    log(f"[rank {rank}] {wl.name}: n={n} m={m} nnz(S1)={sysm.stiff_total.nnz} "
+        f"assembly {t_asm:.1f}s precond setup {t_setup:.1f}s")
+    ion = wl.ionic
+    pts = wl.mesh.vertices[:m]
+    state = bd.SimState.resting(n, m, ion)
+    tol, max_iter = wl.tol, 20000
+
+    def step(s):
+        return bd.time_step(s, sysm, pre, ion, wl.protocol, wl.dt, tol=tol, max_iter=max_iter,
+                            heart_points=pts)
+
+    warm_iters = []
+    for _ in range(args.warmup):
+        state, st = step(state)
+        warm_iters.append(st.iterations)
+    saved = (state.u.clone(), state.v.clone(), state.w.clone(), state.t, state.step)
+    stream = torch.cuda.current_stream(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, dev_ms = [], []
+    e0.record(stream)
+    for _ in range(args.steps):
+        state, st = step(state)
+        iters.append(st.iterations)
+        dev_ms.append(st.device_time_ms)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - launches0
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+    total_iters = sum(iters)
+
+    # ---- e2e: same K steps through the public API with host buffers ----------------
+    u0, v0, w0, t_s, k_s = saved
+    hu = torch.empty(n, dtype=torch.float64).pin_memory()
+    hv = torch.empty(m, dtype=torch.float64).pin_memory()
+    hw = torch.empty(m, dtype=torch.float64).pin_memory()
+    hu.copy_(u0.cpu())
+    hv.copy_(v0.cpu())
+    hw.copy_(w0.cpu())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t_host = t_s
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    e2.record(stream)
+    for k in range(args.steps):
+        s = bd.SimState(u=hu.to(dev, non_blocking=True), v=hv.to(dev, non_blocking=True),
+                        w=hw.to(dev, non_blocking=True), t=t_host, step=k_s + k)
+        s, _ = step(s)
+        hu.copy_(s.u, non_blocking=True)
+        hv.copy_(s.v, non_blocking=True)
+        hw.copy_(s.w, non_blocking=True)
+        t_host = s.t
+    e3.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3)
+    wall_e2e = time.perf_counter() - wall0
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
+    bytes_in = 8 * (n + 2 * m)
+
+    # ---- per-kernel-class profile of one extra step (CUDA events on the library stream) --
+    L = _lib.lib()
+    import ctypes as C
+    L.bd_profile_enable(ctx.handle, 1)
+    st_prof = bd.SimState(u=u0.clone(), v=v0.clone(), w=w0.clone(), t=t_s, step=k_s)
+    _, stp = step(st_prof)
+    times = (C.c_double * 8)()
+    counts = (C.c_int64 * 8)()
+    L.bd_profile_read(ctx.handle, times, counts, 8)
+    L.bd_profile_enable(ctx.handle, 0)
+    classes = ["lambda", "update", "bulk_trsv", "schur_trsv", "si_spmv", "vector", "init"]
+    prof = {c: {"ms": round(times[i], 4), "marks": int(counts[i])} for i, c in enumerate(classes)}
+    prof_total = sum(times[i] for i in range(7))
+
+    # algorithmic bytes
+    info_b = pre.inner_bulk.factor_info() if wl.inner != "jacobi" else {"nnz": n, "levels": 1}
+    info_k = pre.inner_schur.factor_info() if wl.inner != "jacobi" else {"nnz": m, "levels": 1}
+    peak, peak_kind = measured_peak_hbm()
+    n_bulk_solves = 2 * (stp.iterations + 1)  # two bulk solves per P^{-1} application
+    bulk_ms = times[2] / max(n_bulk_solves, 1)
+    solve_bytes = 2 * tri_bytes(info_b["nnz"], n)  # forward + backward pass
+    achieved = solve_bytes / (bulk_ms * 1e-3) / 1e9 if bulk_ms > 0 else None
+    b_iter = iteration_bytes(n, m, sysm.stiff_total.nnz, sysm.stiff_intra.nnz, info_b["nnz"],
+                             info_k["nnz"])
+    ms_per_iter = ms_per_step / (total_iters / args.steps)
+    traffic = None
+    ncu_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_path):
+        with open(ncu_path) as fh:
+            traffic = json.load(fh).get(f"{wl.name}_{wl.inner}_bulk_solve_bytes")
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(sysm, km, wl, np.mean(iters), args.cpu_iters)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic structured mesh, seeded/defined stimulus; "
+                    "no dataset)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "dof": n + m, "n": n,
+                       "n_heart": m, "inner": wl.inner, "tol": wl.tol, "dt_ms": wl.dt,
+                       "steps_timed": f"{args.warmup + 1}..{args.warmup + args.steps}",
+                       "pcg_iters_per_step": round(total_iters / args.steps, 2),
+                       "ms_per_pcg_iter": round(ms_per_iter, 4),
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "inputs > L2 (≈%.2f GB streamed per PCG iteration)" % (b_iter / 1e9)},
+            "e2e": {"value": round(e2e_value, 4), "unit": UNIT,
+                    "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_in,
+                    "wall_s": round(wall_e2e, 3)},
+            "roofline": {"bound": "hbm",
+                         "kernel": "bulk IC(0) triangular solve pair (k_trsv_fwd + k_trsv_bwd, "
+                                   "P_1 block)" if wl.inner != "jacobi" else "jacobi",
+                         "achieved": round(achieved, 1) if achieved else None,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None,
+                         "peak_source": peak_kind,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_launch": solve_bytes,
+                         "avg_launch_ms": round(bulk_ms, 5),
+                         "levels": info_b["levels"],
+                         "iteration": {"bytes": b_iter, "ms": round(ms_per_iter, 4),
+                                       "achieved_gbs": round(b_iter / (ms_per_iter * 1e-3) / 1e9, 1),
+                                       "frac": round(b_iter / (ms_per_iter * 1e-3) / 1e9 / peak, 4)}},
+            "profile_ms": prof, "profile_step_ms": round(prof_total, 3),
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "setup_s": {"assembly": round(t_asm, 1), "precond": round(t_setup, 2)},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(sysm, km, wl, iters_per_step, n_iter):
+    """Oracle port, 1 thread: time a bounded number of PCG iterations of the
+    same workload's first step and extrapolate with the iterations per step."""
+    from oracle import bidomain_oracle as orc
+    from paper_1711_08708_b200.ionic import stimulus_vector
+    t0 = time.perf_counter()
+    pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, wl.inner)
+    t_setup = time.perf_counter() - t0
+    m, n = sysm.n_heart, sysm.n
+    v = np.full(m, wl.ionic.v_rest)
+    w = np.ones(m)
+    ion = orc.ionic_current(v, w, c_m=wl.params.c_m)
+    stim = stimulus_vector(wl.mesh.vertices[:m], 0.0, wl.protocol)
+    bu, bv = orc.build_rhs(n, sysm.heart_mass_diag, sysm.gamma, v, ion, stim, wl.params.chi)
+    t0 = time.perf_counter()
+    try:
+        orc.pcg(sysm.stiff_total, sysm.stiff_intra, sysm.heart_mass_diag, sysm.mass_diag,
+                sysm.gamma, pre, bu, bv, tol=wl.tol, max_iter=n_iter, x0=(np.zeros(n), v))
+        done = None
+    except orc.OracleNoConvergence as exc:
+        done = exc.stats["iterations"]
+    dt = time.perf_counter() - t0
+    k = done if done else n_iter
+    per_iter = dt / (k + 1)  # k loop iterations + the initial residual/P^{-1}
+    step_s = per_iter * iters_per_step
+    return {"value": round(1.0 / step_s, 6), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{k} PCG iterations (+initial P^-1) of step 1 of {wl.name} with the "
+                      f"oracle (scipy spsolve_triangular / csr matvec, 1 thread), "
+                      f"{per_iter * 1e3:.1f} ms/iter, extrapolated x{iters_per_step:.1f} "
+                      f"it/step; oracle setup {t_setup:.1f}s excluded",
+            "host_cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} cpus)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} cpus"
+
+
+# ---------------------------------------------------------------------------------
+def run_reference(args, rank):
+    """CPU reference arm: the oracle port on this host's cores, bounded samples."""
+    if rank != 0:
+        return
+    from oracle import bidomain_oracle as orc
+    from paper_1711_08708_b200.ionic import stimulus_vector
+    wl = build_workload(args.workload, args.inner)
+    sysm, km, t_asm = assemble(wl)
+    pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, wl.inner)
+    n, m = sysm.n, sysm.n_heart
+    fx = os.path.join(REPO, "tests", "golden", f"{wl.name}_{wl.inner}_oracle.json")
+    ref_iters = None
+    if os.path.exists(fx):
+        with open(fx) as fh:
+            ref_iters = json.load(fh)["iters"]
+    state = (np.zeros(n), np.full(m, wl.ionic.v_rest), np.ones(m))
+    pts = wl.mesh.vertices[:m]
+    step_times, used = [], []
+    sample = args.cpu_iters
+    for k in range(args.warmup + args.steps):
+        t = k * wl.dt
+        stim = stimulus_vector(pts, t, wl.protocol)
+        u, v, w = state
+        ion = orc.ionic_current(v, w, c_m=wl.params.c_m)
+        bu, bv = orc.build_rhs(n, sysm.heart_mass_diag, sysm.gamma, v, ion, stim, wl.params.chi)
+        t0 = time.perf_counter()
+        try:
+            (un, vn), st = orc.pcg(sysm.stiff_total, sysm.stiff_intra, sysm.heart_mass_diag,
+                                   sysm.mass_diag, sysm.gamma, pre, bu, bv, tol=wl.tol,
+                                   max_iter=sample, x0=(u, v))
+            kk = st["iterations"]
+        except orc.OracleNoConvergence as exc:
+            kk = exc.stats["iterations"]
+            un, vn = u, v
+        dt = time.perf_counter() - t0
+        per_iter = dt / (kk + 1)
+        if ref_iters and k < len(ref_iters):
+            it = ref_iters[k]
+        elif ref_iters:
+            it = float(np.mean(ref_iters))
+        else:
+            it = float("nan")
+        if k >= args.warmup:
+            step_times.append(per_iter * it)
+            used.append(it)
+        w = orc.update_gate(w, vn, wl.dt)
+        state = (u, v, w)  # bounded sample: the potential is not advanced
+    total = float(np.sum(step_times))
+    value = args.steps / total if total > 0 else None
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6) if value else None,
+            "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic structured mesh)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "dof": n + m,
+                       "inner": wl.inner, "tol": wl.tol,
+                       "pcg_iters_per_step": round(float(np.mean(used)), 2) if used else None},
+            "cpu_baseline": {"value": round(value, 6) if value else None, "unit": UNIT,
+                             "cores": 1, "kind": "port",
+                             "sample": f"each step: {sample} PCG iterations of the oracle port "
+                                       f"(scipy sparse kernels are single-threaded), per-iteration "
+                                       f"time x the oracle's own iterations for that step "
+                                       f"({os.path.basename(fx)})",
+                             "host_cpu": _cpu_model()},
+            "e2e": {"value": round(value, 6) if value else None, "unit": UNIT,
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": {"assembly": round(t_asm, 1)}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--inner", default=None)
+    ap.add_argument("--cpu-iters", type=int, default=6)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_native(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

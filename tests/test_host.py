@@ -1,0 +1,167 @@
+"""CPU: the C-ABI library loads and exports every declared symbol; host-side
+setup (meshes, assembly, configs, stimulus masks) is consistent with the
+golden inputs and, where the reference is importable, with the reference."""
+import os
+import re
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import REPO, csr, golden
+
+import paper_1711_08708_b200 as bd
+from paper_1711_08708_b200 import _lib, configs
+from paper_1711_08708_b200.ionic import active_sites, site_masks
+
+HEADER = os.path.join(REPO, "include", "bidomain_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(bd_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load_library()
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    for s in syms:
+        assert hasattr(lib, s), f"{s} not exported by {_lib.LIB_NAME}"
+        assert s in bound, f"{s} not bound in _lib.SIGNATURES"
+    assert lib.bd_version().decode().endswith("sm_100a")
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_error_mapping():
+    with pytest.raises(ValueError):
+        _lib.check(_lib.BD_EINVAL)
+    with pytest.raises(bd.PreconditionerError):
+        _lib.check(_lib.BD_EPRECOND)
+    with pytest.raises(bd.NonConvergenceError) as e:
+        _lib.check(_lib.BD_ENOCONV, stats="s")
+    assert e.value.stats == "s"
+    with pytest.raises(bd.NumericalBreakdownError):
+        _lib.check(_lib.BD_EBREAKDOWN)
+
+
+def test_no_cuda_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_lib.NativeUnavailableError):
+        _lib.Context(0)
+
+
+def test_unknown_inner_name():
+    with pytest.raises(ValueError):
+        bd.make_inner("amg")
+
+
+def test_gamma():
+    assert bd.gamma(500.0, 1.0, 0.2) == pytest.approx(2500.0)
+    assert bd.gamma(200.0, 1.0, 0.05) == pytest.approx(4000.0)
+    with pytest.raises(ValueError):
+        bd.gamma(500.0, 1.0, 0.0)
+
+
+@pytest.mark.parametrize("case", ["cfg0", "cfg2s"])
+def test_assembly_matches_golden_inputs(case):
+    """This repo's builders + assembly reproduce the matrices the reference
+    assembled for the golden runs (same pattern, values to 1e-14)."""
+    if case == "cfg0":
+        wl = configs.cfg0(64)
+    else:
+        wl = configs.cfg2((12, 12, 6))
+    g = golden(case)
+    sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers)
+    km = bd.build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+    for key, mat in (("S1", sysm.stiff_total), ("Si", sysm.stiff_intra), ("Km", km)):
+        ref = csr(g, key)
+        assert np.array_equal(mat.indptr, ref.indptr) and np.array_equal(mat.indices, ref.indices)
+        np.testing.assert_allclose(mat.data, ref.data, rtol=0, atol=1e-14 * np.abs(ref.data).max())
+    np.testing.assert_allclose(sysm.mass_diag, g["mass"], rtol=1e-15)
+    assert sysm.gamma == float(g["gamma"])
+
+
+def test_cfg1_small_matches_golden_inputs():
+    wl = configs.cfg1(64)
+    g = golden("cfg1s")
+    assert np.array_equal(wl.mesh.tags, g["tags"])
+    assert wl.mesh.heart_vertex_count == int(g["n_heart"])
+    sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers)
+    ref = csr(g, "S1")
+    np.testing.assert_allclose(sysm.stiff_total.toarray(), ref.toarray(), rtol=0,
+                               atol=1e-13 * np.abs(ref.data).max())
+
+
+def test_config_sizes():
+    # vertex counts from the BASELINE text (cfg2: 129*129*65, cfg1: 513^2)
+    assert (128 + 1) * (128 + 1) * (64 + 1) == 1081665
+    wl = configs.cfg1(64)
+    assert wl.mesh.vertex_count == 65 * 65
+    assert 0 < wl.mesh.heart_vertex_count < wl.mesh.vertex_count
+    wl = configs.cfg2((8, 8, 4))
+    assert wl.mesh.vertex_count == 9 * 9 * 5 and wl.n_heart == wl.n
+    wl.mesh.validate()
+
+
+def test_ellipsoid_mesh_small():
+    mesh = bd.build_ellipsoid_torso_3d(16, validate=True)
+    assert 0 < mesh.heart_vertex_count < mesh.vertex_count
+    assert set(np.unique(mesh.tags)) <= {0, 2, 3}
+
+
+def test_stimulus_masks_match_vector():
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(0, 1, (500, 2))
+    proto = bd.StimulusProtocol(sites=(bd.StimulusSite((0.3, 0.4)),
+                                       bd.StimulusSite((0.7, 0.6), start=5.0),
+                                       bd.StimulusBox((-np.inf, -np.inf), (0.1, np.inf))),
+                                radius=0.2, amplitude=140.0, duration=2.0)
+    masks = site_masks(pts, proto)
+    for t in (0.0, 1.99, 2.0, 5.0, 6.5, 7.0):
+        act = active_sites(t, proto)
+        vec = np.where((masks & np.uint64(act)) != 0, proto.amplitude, 0.0)
+        assert np.array_equal(vec, bd.stimulus_vector(pts, t, proto))
+
+
+def test_fiber_frames_orthonormal():
+    rng = np.random.default_rng(1)
+    c = rng.uniform(0, 20, (200, 3))
+    for model in (bd.TransmuralRotation(), bd.EllipsoidHelical((10, 10, 10), (5, 4, 4), 1.0)):
+        fr = model.frames(c)
+        gram = np.einsum("nij,nkj->nik", fr, fr)
+        np.testing.assert_allclose(gram, np.broadcast_to(np.eye(3), gram.shape), atol=1e-12)
+
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not mounted (GPU box)")
+def test_builders_and_assembly_bit_identical_to_reference():
+    sys.path.insert(0, os.path.join(REPO, "tests", "golden"))
+    import refshim
+    R = refshim.import_reference()
+    for f in ("build_cube_mesh", "build_square_mesh", "build_heart_torso_2d"):
+        for m in (4, 8):
+            a, b = getattr(R, f)(m), getattr(bd, f)(m)
+            assert np.array_equal(a.vertices, b.vertices) and np.array_equal(a.elements, b.elements)
+            assert np.array_equal(a.tags, b.tags) and a.heart_vertex_count == b.heart_vertex_count
+    for mr, mb, d, dt in ((R.build_heart_torso_2d(8), bd.build_heart_torso_2d(8), 2, 0.05),
+                          (R.build_cube_mesh(4), bd.build_cube_mesh(4), 3, 0.2)):
+        sr = R.BidomainSystem.build(mr, R.default_params(d), dt)
+        sb = bd.BidomainSystem.build(mb, bd.default_params(d), dt)
+        for k in ("stiff_total", "stiff_intra", "stiff_extra"):
+            x, y = getattr(sr, k), getattr(sb, k)
+            assert np.array_equal(x.indices, y.indices) and np.array_equal(x.data, y.data)
+        kr = R.build_monodomain_matrix(mr, R.default_params(d), sr.gamma)
+        kb = bd.build_monodomain_matrix(mb, bd.default_params(d), sb.gamma)
+        assert np.array_equal(kr.data, kb.data)
