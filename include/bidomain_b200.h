@@ -111,6 +111,13 @@ bd_status bd_system_weighted_mean_u(bd_system* s, const double* u, double* out);
 bd_status bd_inner_create(bd_ctx* ctx, int kind, int64_t n, const int64_t* indptr,
                           const int32_t* indices, const double* values, int max_restarts,
                           bd_inner** out, int* restarts_used);
+/* As bd_inner_create, with optional vertex coordinates (row-major n×dim,
+ * host) used only to partition the rows of the tiled triangular-solve
+ * schedule (coordinate bisection); NULL falls back to a graph bisection.
+ * The factor itself does not depend on them. */
+bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* indptr,
+                             const int32_t* indices, const double* values, int max_restarts,
+                             const double* coords, int dim, bd_inner** out, int* restarts_used);
 bd_status bd_inner_destroy(bd_inner* p);
 /* z = P^{-1} y (device pointers, length n). */
 bd_status bd_inner_apply(bd_inner* p, const double* y, double* z);

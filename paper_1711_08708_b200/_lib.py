@@ -59,6 +59,8 @@ SIGNATURES = [
     ("bd_system_weighted_mean_u", _i32, [_vp, _vp, C.POINTER(_dbl)]),
     ("bd_inner_create", _i32, [_vp, C.c_int, _i64, _vp, _vp, _vp, C.c_int, _pp,
                                C.POINTER(C.c_int)]),
+    ("bd_inner_create_ex", _i32, [_vp, C.c_int, _i64, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _pp,
+                                  C.POINTER(C.c_int)]),
     ("bd_inner_destroy", _i32, [_vp]),
     ("bd_inner_apply", _i32, [_vp, _vp, _vp]),
     ("bd_inner_factor_info", _i32, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),

@@ -65,12 +65,50 @@ struct DevTri {
   dev::Tri dev() const { return dev::Tri{n, rowptr, col, val, tasks, ntasks}; }
 };
 
+struct DevTile {
+  int* part_task_ptr = nullptr;
+  int* part_step_ptr = nullptr;
+  int* step_task_ptr = nullptr;
+  int* task_row = nullptr;
+  double* task_diag = nullptr;
+  int* ell_col = nullptr;
+  double* ell_val = nullptr;
+  int max_part_rows = 0;
+  int max_part_steps = 0;
+  int nsteps = 0;
+  dev::TileDev dev() const {
+    return dev::TileDev{part_task_ptr, part_step_ptr, step_task_ptr, task_row, task_diag,
+                        ell_col,       ell_val,       max_part_rows, max_part_steps};
+  }
+};
+
+constexpr int kTileStages = 8;
+
+struct DevEll {
+  int* task_row = nullptr;
+  double* task_diag = nullptr;
+  int* ell_col = nullptr;
+  double* ell_val = nullptr;
+  int ntasks = 0;
+  int nchunks = 0;
+  int grid = 0;
+  dev::EllTri dev() const { return dev::EllTri{task_row, task_diag, ell_col, ell_val, ntasks}; }
+};
+
 struct bd_inner {
   bd_ctx* ctx;
   int kind;
   int64_t n;
   int G = 8;
   DevTri L, U;
+  // tiled cooperative schedule (IC(0) factors with short rows)
+  bool tiled = false;
+  bool persist = false;
+  DevEll EL, EU;
+  int TG = 8, tparts = 0, tthreads = 0, tstages = 8, trows = 128;
+  bool rows_mode = false;
+  size_t tsmem = 0;
+  DevTile TL, TU;
   int* perm = nullptr;        // exact: new -> old
   double* inv = nullptr;      // jacobi
   double* y_int = nullptr;    // forward output (sentinel between solves)
@@ -131,6 +169,12 @@ bd_status fail(bd_ctx* ctx, bd_status st, const std::string& msg) {
     cudaError_t e_ = cudaGetLastError();                                                \
     if (e_ != cudaSuccess)                                                              \
       return fail((ctx), BD_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    bd_status st_ = (expr);       \
+    if (st_ != BD_OK) return st_; \
   } while (0)
 
 template <class T>
@@ -253,6 +297,179 @@ void free_tri(DevTri* t) {
   cudaFree(t->tasks);
 }
 
+template <class T>
+cudaError_t upload_vec(T** dst, const std::vector<T>& v) {
+  cudaError_t e = dalloc(dst, (int64_t)v.size());
+  if (e) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
+bd_status upload_tile(bd_ctx* ctx, const TileSchedule& ts, DevTile* out) {
+  CK(ctx, upload_vec(&out->part_task_ptr, ts.part_task_ptr));
+  CK(ctx, upload_vec(&out->part_step_ptr, ts.part_step_ptr));
+  CK(ctx, upload_vec(&out->step_task_ptr, ts.step_task_ptr));
+  CK(ctx, upload_vec(&out->task_row, ts.task_row));
+  CK(ctx, upload_vec(&out->task_diag, ts.task_diag));
+  CK(ctx, upload_vec(&out->ell_col, ts.ell_col));
+  CK(ctx, upload_vec(&out->ell_val, ts.ell_val));
+  out->max_part_rows = ts.max_part_rows;
+  out->max_part_steps = ts.max_part_steps;
+  out->nsteps = (int)ts.step_task_ptr.size() - 1;
+  return BD_OK;
+}
+
+void free_tile(DevTile* t) {
+  cudaFree(t->part_task_ptr);
+  cudaFree(t->part_step_ptr);
+  cudaFree(t->step_task_ptr);
+  cudaFree(t->task_row);
+  cudaFree(t->task_diag);
+  cudaFree(t->ell_col);
+  cudaFree(t->ell_val);
+}
+
+// Build the tiled schedules of an IC(0)-like factor; leaves p->tiled false if
+// a row is too long or the part does not fit in shared memory.
+bd_status setup_tiles(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
+                      const double* coords, int dim) {
+  bd_ctx* ctx = p->ctx;
+  const char* env = getenv("BD_NO_TILE");
+  if (env && env[0] == '1') return BD_OK;
+  int64_t maxoff = 0;
+  for (int64_t i = 0; i < lower.n; ++i)
+    maxoff = std::max<int64_t>(maxoff, lower.indptr[i + 1] - lower.indptr[i] - 1);
+  for (int64_t i = 0; i < upper.n; ++i)
+    maxoff = std::max<int64_t>(maxoff, upper.indptr[i + 1] - upper.indptr[i] - 1);
+  int G = 4;
+  while (G < maxoff) G <<= 1;
+  if (G > 16) return BD_OK;
+  int threads = std::min(1024, 128 * G);
+  if (const char* e = getenv("BD_TILE_THREADS")) threads = atoi(e);
+  int R = threads / G;
+  if (p->rows_mode) {
+    R = getenv("BD_TILE_ROWS") ? atoi(getenv("BD_TILE_ROWS")) : 128;
+    threads = 512;
+  }
+  int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nsm, lower.n / 1024));
+  if (const char* e = getenv("BD_TILE_PARTS")) parts = std::max(1, atoi(e));
+  std::vector<int32_t> part;
+  if (coords && dim > 0)
+    partition_coords(lower.n, dim, coords, parts, &part);
+  else
+    partition_rows(lower, parts, &part);
+  TileSchedule tl, tu;
+  if (!build_tile_schedule(lower, true, part, parts, G, R, &tl, p->rows_mode)) return BD_OK;
+  if (!build_tile_schedule(upper, false, part, parts, G, R, &tu, p->rows_mode)) return BD_OK;
+  const int mrows = std::max(tl.max_part_rows, tu.max_part_rows);
+  const int msteps = std::max(tl.max_part_steps, tu.max_part_steps);
+  const int stages = getenv("BD_TILE_D") ? atoi(getenv("BD_TILE_D")) : kTileStages;
+  const size_t smem = p->rows_mode ? dev::tile2_smem_bytes(mrows, msteps, R, G, stages)
+                                   : dev::tile_smem_bytes(mrows, msteps, threads, G, stages);
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (smem + 1024 > (size_t)max_smem) return BD_OK;  // 1 KB headroom for static smem
+  TRY(upload_tile(ctx, tl, &p->TL));
+  TRY(upload_tile(ctx, tu, &p->TU));
+  p->TL.max_part_rows = p->TU.max_part_rows = mrows;
+  p->TL.max_part_steps = p->TU.max_part_steps = msteps;
+  p->TG = G;
+  p->tparts = parts;
+  p->tthreads = threads;
+  p->tsmem = smem;
+  p->tstages = stages;
+  p->trows = R;
+  p->tiled = true;
+  return BD_OK;
+}
+
+// ELL, level-ordered schedule for the persistent sync-free kernel.
+bd_status build_ell(bd_ctx* ctx, const HostCsr& t, bool lower, int G, DevEll* out) {
+  std::vector<int32_t> level, tasks;
+  const int64_t depth = row_levels(t, lower, &level);
+  build_schedule(level, depth, 32 / G, &tasks);
+  const int64_t nt = (int64_t)tasks.size();
+  std::vector<double> diag(nt, 1.0), val(nt * G, 0.0);
+  std::vector<int32_t> col(nt * G, -1);
+  for (int64_t k = 0; k < nt; ++k) {
+    const int32_t row = tasks[k];
+    if (row < 0) continue;
+    int cnt = 0;
+    for (int64_t q = t.indptr[row]; q < t.indptr[row + 1]; ++q) {
+      const int32_t cidx = t.indices[q];
+      if (cidx == row) {
+        diag[k] = t.values[q];
+        continue;
+      }
+      if (cnt == G) return BD_EINVAL;
+      col[k * G + cnt] = cidx;
+      val[k * G + cnt] = t.values[q];
+      ++cnt;
+    }
+  }
+  CK(ctx, upload_vec(&out->task_row, tasks));
+  CK(ctx, upload_vec(&out->task_diag, diag));
+  CK(ctx, upload_vec(&out->ell_col, col));
+  CK(ctx, upload_vec(&out->ell_val, val));
+  out->ntasks = (int)nt;
+  const int rpc = dev::TPB / G;
+  out->nchunks = (int)((nt + rpc - 1) / rpc);
+  // ~3 levels of rows in flight
+  const int64_t rows_flight = 3 * std::max<int64_t>(1, t.n / std::max<int64_t>(1, depth));
+  const char* env = getenv("BD_PERSIST_LEVELS");
+  const int64_t lv = env ? std::max(1, atoi(env)) : 3;
+  const int64_t want = (lv * std::max<int64_t>(1, t.n / std::max<int64_t>(1, depth)) + rpc - 1) / rpc;
+  (void)rows_flight;
+  out->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->nsm * 8));
+  out->grid = std::min(out->grid, out->nchunks);
+  return BD_OK;
+}
+
+void free_ell(DevEll* e) {
+  cudaFree(e->task_row);
+  cudaFree(e->task_diag);
+  cudaFree(e->ell_col);
+  cudaFree(e->ell_val);
+}
+
+template <int G, class Rhs>
+bd_status launch_tiled(bd_inner* p, const DevTile& t, const Rhs& rhs, double* xg, const Ctl& c,
+                       int ctr, int fin, int slot, int slot2, int64_t nmean) {
+  bd_ctx* ctx = p->ctx;
+  if (p->rows_mode) {
+    auto kr = dev::k_trsv_rows<G, kTileStages, Rhs>;
+    CK(ctx, cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tsmem));
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cudaLaunchConfig_t cf = {};
+    cf.gridDim = dim3(p->tparts);
+    cf.blockDim = dim3(p->tthreads);
+    cf.dynamicSmemBytes = p->tsmem;
+    cf.stream = ctx->stream;
+    cf.attrs = at;
+    cf.numAttrs = 1;
+    CK(ctx, cudaLaunchKernelEx(&cf, kr, t.dev(), rhs, xg, c, ctr, fin, slot, slot2, nmean, p->trows));
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
+  auto kern = p->tstages >= 16 ? dev::k_trsv_tiled<G, 16, Rhs> : dev::k_trsv_tiled<G, kTileStages, Rhs>;
+  CK(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tsmem));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->tparts);
+  cfg.blockDim = dim3(p->tthreads);
+  cfg.dynamicSmemBytes = p->tsmem;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(ctx, cudaLaunchKernelEx(&cfg, kern, t.dev(), rhs, xg, c, ctr, fin, slot, slot2, nmean));
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
 // ---- inner solve dispatch -----------------------------------------------------
 // Solve P x = rhs for one inner preconditioner inside control block c.
 // x_int: polled internal output (sentinel-filled here); out (nullable):
@@ -268,6 +485,41 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->persist) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_persist<G, Rhs><<<p->EL.grid, dev::TPB, 0, st>>>(
+        p->EL.dev(), rhs, p->y_int, c, ctr0, ctr0 + 1, p->EL.nchunks, -1, 0, -1, 1);
+    LAUNCHED(ctx);
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_persist<G, dev::RhsGather><<<p->EU.grid, dev::TPB, 0, st>>>(
+        p->EU.dev(), dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, p->EU.nchunks, fin, slot,
+        slot2, nmean);
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->tiled) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    switch (p->TG) {
+      case 4:
+        TRY(launch_tiled<4>(p, p->TL, rhs, p->y_int, c, ctr0, -1, 0, -1, 1));
+        TRY(launch_tiled<4>(p, p->TU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 3, fin, slot, slot2,
+                            nmean));
+        break;
+      case 8:
+        TRY(launch_tiled<8>(p, p->TL, rhs, p->y_int, c, ctr0, -1, 0, -1, 1));
+        TRY(launch_tiled<8>(p, p->TU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 3, fin, slot, slot2,
+                            nmean));
+        break;
+      default:
+        TRY(launch_tiled<16>(p, p->TL, rhs, p->y_int, c, ctr0, -1, 0, -1, 1));
+        TRY(launch_tiled<16>(p, p->TU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 3, fin, slot,
+                             slot2, nmean));
+    }
     return BD_OK;
   }
   dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(x_int, p->n, dev::SENTINEL, c);
@@ -340,12 +592,6 @@ bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
   LAUNCHED(ctx);
   return BD_OK;
 }
-
-#define TRY(expr)                 \
-  do {                            \
-    bd_status st_ = (expr);       \
-    if (st_ != BD_OK) return st_; \
-  } while (0)
 
 // P_Λ^{-1} r (bd/precond.py:298-312) with sc[MU1], sc[C1] already holding
 // mean(r_u) and mean(r_u)/beta.  zu: output u-block; zv_int: polled Schur
@@ -708,6 +954,13 @@ bd_status bd_system_weighted_mean_u(bd_system* s, const double* u, double* out) 
 bd_status bd_inner_create(bd_ctx* ctx, int kind, int64_t n, const int64_t* indptr,
                           const int32_t* indices, const double* values, int max_restarts,
                           bd_inner** out, int* restarts_used) {
+  return bd_inner_create_ex(ctx, kind, n, indptr, indices, values, max_restarts, nullptr, 0, out,
+                            restarts_used);
+}
+
+bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* indptr,
+                             const int32_t* indices, const double* values, int max_restarts,
+                             const double* coords, int dim, bd_inner** out, int* restarts_used) {
   if (!ctx || !out || n <= 0 || !indptr) return fail(ctx, BD_EINVAL, "bd_inner_create: bad arguments");
   if (kind != BD_INNER_EXACT && kind != BD_INNER_IC0 && kind != BD_INNER_JACOBI)
     return fail(ctx, BD_EINVAL, "unknown inner preconditioner kind");
@@ -778,6 +1031,25 @@ bd_status bd_inner_create(bd_ctx* ctx, int kind, int64_t n, const int64_t* indpt
   p->G = pick_g(avg - 1.0);
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
+  if (st == BD_OK && kind == BD_INNER_IC0) {
+    const char* mode = getenv("BD_TRSV");
+    const std::string m = mode ? mode : "persist";
+    if (m == "tiled" || m == "rows") {
+      p->rows_mode = (m == "rows");
+      st = setup_tiles(p, lower, upper, coords, dim);
+    } else if (m == "persist") {
+      int64_t maxoff = 0;
+      for (int64_t i = 0; i < n; ++i)
+        maxoff = std::max<int64_t>(maxoff, lower.indptr[i + 1] - lower.indptr[i] - 1);
+      for (int64_t i = 0; i < n; ++i)
+        maxoff = std::max<int64_t>(maxoff, upper.indptr[i + 1] - upper.indptr[i] - 1);
+      if (maxoff <= p->G) {
+        st = build_ell(ctx, lower, true, p->G, &p->EL);
+        if (st == BD_OK) st = build_ell(ctx, upper, false, p->G, &p->EU);
+        if (st == BD_OK) p->persist = true;
+      }
+    }
+  }
   if (st != BD_OK) {
     bd_inner_destroy(p);
     return st;
@@ -806,6 +1078,10 @@ bd_status bd_inner_destroy(bd_inner* p) {
   cudaStreamSynchronize(p->ctx->stream);
   free_tri(&p->L);
   free_tri(&p->U);
+  free_tile(&p->TL);
+  free_tile(&p->TU);
+  free_ell(&p->EL);
+  free_ell(&p->EU);
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);
@@ -821,6 +1097,28 @@ bd_status bd_inner_apply(bd_inner* p, const double* y, double* z) {
   dev::RhsVec rhs{y, (int)p->n, nullptr, p->perm};
   if (p->kind == BD_INNER_JACOBI) return inner_solve(p, rhs, z, nullptr, p->ctl, dev::C_JAC1);
   return inner_solve(p, rhs, p->x_int, z, p->ctl, dev::C_BULK1_S);
+}
+
+// Debug: enable the tiled-solve step trace (buffer of parts*steps*3 u64 on the
+// device; NULL disables).  Not part of the public header.
+bd_status bd_debug_tile_trace(void* dev_buf, int steps) {
+  cudaMemcpyToSymbol(dev::g_tile_trace, &dev_buf, sizeof(void*));
+  cudaMemcpyToSymbol(dev::g_tile_trace_steps, &steps, sizeof(int));
+  return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ECUDA;
+}
+
+bd_status bd_inner_tile_info(bd_inner* p, int64_t* info) {
+  // parts, threads, G, smem, max_part_rows, max_part_steps, L nsteps, U nsteps
+  if (!p) return BD_EINVAL;
+  info[0] = p->tiled ? p->tparts : 0;
+  info[1] = p->tthreads;
+  info[2] = p->TG;
+  info[3] = (int64_t)p->tsmem;
+  info[4] = p->TL.max_part_rows;
+  info[5] = p->TL.max_part_steps;
+  info[6] = p->TL.nsteps;
+  info[7] = p->TU.nsteps;
+  return BD_OK;
 }
 
 bd_status bd_inner_factor_info(bd_inner* p, int64_t* n, int64_t* nnz, int64_t* levels) {
@@ -865,6 +1163,7 @@ bd_status bd_blocklu_create(bd_system* s, bd_inner* bulk, bd_inner* schur, doubl
   const int64_t n = s->n, m = s->m, nm = n + m;
   int64_t parts = (int64_t)ctx->nsm * 8 * 2;
   parts = std::max<int64_t>(parts, std::max(bulk->U.nvb, schur->U.nvb));
+  parts = std::max<int64_t>(parts, std::max(bulk->EU.nchunks, schur->EU.nchunks));
   p->hist_cap = 0;
   if (ctl_alloc(&p->ctl, parts, 0, 1) || dalloc(&p->traw, n) || dalloc(&p->z2raw, n) ||
       dalloc(&p->corr, m) || dalloc(&p->sbuf, m) || dalloc(&p->x, nm) || dalloc(&p->r, nm) ||

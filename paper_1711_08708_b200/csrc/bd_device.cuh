@@ -7,6 +7,7 @@
 // control flags and return when the solve is finished, so an iteration can be
 // enqueued (or replayed from a CUDA graph) without a host round trip.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(TPB) k_update(double* x, double* r, const doub
 // `y - y.mean()` of _bulk_inverse (bd/precond.py:289-290); perm for the
 // fill-reducing ordering of the exact factor.
 struct RhsVec {
+  static constexpr bool kScalar = true;
   const double* src;
   int src_len;
   const double* shift;
@@ -419,6 +421,7 @@ struct RhsVec {
 // fly: `rhs.v - stiff_intra @ t[:nh]` (bd/precond.py:307) fused with the
 // recentring of the first bulk solve (:291-292).
 struct RhsSchur {
+  static constexpr bool kScalar = false;
   Csr si;
   const double* traw;
   const double* sc;
@@ -567,6 +570,593 @@ __global__ void __launch_bounds__(TPB) k_trsv_bwd(Tri t, double* __restrict__ yi
         c.ctr[ctr_done] = 0u;
         __threadfence();
       }
+    }
+  }
+}
+
+// ---- tiled cooperative triangular solve -----------------------------------
+// One CTA per row part (graph partition of the factor's pattern); the part's
+// rows are processed in level order, one level chunk ("step") per
+// __syncthreads.  Dependencies inside the part are read from shared memory
+// (xs holds the right-hand side, overwritten in place by the solution);
+// dependencies on other parts are polled in global memory (sentinel).  The
+// ELL entries of upcoming steps stream into a D-stage shared-memory ring with
+// cp.async, issued D-1 steps ahead, so the step loop never waits on HBM.
+struct TileDev {
+  const int* part_task_ptr;
+  const int* part_step_ptr;
+  const int* step_task_ptr;
+  const int* task_row;
+  const double* task_diag;
+  const int* ell_col;
+  const double* ell_val;
+  int max_part_rows;
+  int max_part_steps;
+};
+
+struct RhsGather {  // backward pass: the forward output
+  static constexpr bool kScalar = true;
+  const double* src;
+  template <int G>
+  __device__ __forceinline__ double eval(int row, int) const {
+    return row < 0 ? 0.0 : src[row];
+  }
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int TILE_INVALID = (int)0x80000000;
+
+// Optional step trace (debug): per CTA and step, [globaltimer at step top,
+// spin-poll iterations in the step, globaltimer after the barrier].
+__device__ unsigned long long* g_tile_trace = nullptr;
+__device__ int g_tile_trace_steps = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}  // ring slot of a group with no row this step
+
+__host__ __device__ constexpr size_t tile_ring_offset(int max_rows, int max_steps) {
+  return (((size_t)(max_rows + 1) * 8 + (size_t)(max_steps + 1) * 4) + 15) & ~(size_t)15;
+}
+__host__ __device__ constexpr size_t tile_smem_bytes(int max_rows, int max_steps, int threads,
+                                                     int G, int D) {
+  return tile_ring_offset(max_rows, max_steps) + (size_t)D * threads * 12 +
+         (size_t)D * (threads / G) * 12;
+}
+
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  long long b;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  return __longlong_as_double(b);
+}
+
+template <int G, int D, class Rhs>
+__global__ void __launch_bounds__(1024, 1) k_trsv_tiled(TileDev T, Rhs rhs, double* __restrict__ xg,
+                                                        Ctl c, int ctr, int fin, int slot,
+                                                        int slot2, int64_t nmean) {
+  static_assert(D >= 3, "ring needs >= 3 stages");
+  if (inactive(c)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double sm[32];
+  const int R = blockDim.x / G;
+  const int p = blockIdx.x;
+  const int t0 = T.part_task_ptr[p], t1 = T.part_task_ptr[p + 1];
+  const int nrows = t1 - t0;
+  const int s0 = T.part_step_ptr[p], nst = T.part_step_ptr[p + 1] - s0;
+  double* xs = reinterpret_cast<double*>(smem_raw);
+  int* steps = reinterpret_cast<int*>(xs + T.max_part_rows + 1);
+  double* rv = reinterpret_cast<double*>(smem_raw + tile_ring_offset(T.max_part_rows, T.max_part_steps));
+  int* rc = reinterpret_cast<int*>(rv + (size_t)D * blockDim.x);
+  double* rd = reinterpret_cast<double*>(rc + (size_t)D * blockDim.x);
+  int* rr = reinterpret_cast<int*>(rd + (size_t)D * R);
+  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+
+  // prologue: step table, right-hand side of the own rows into xs, sentinel into xg
+  for (int k = threadIdx.x; k <= nst; k += blockDim.x) steps[k] = T.step_task_ptr[s0 + k];
+  if constexpr (Rhs::kScalar) {
+    // thread per row, 4 independent rows in flight per thread
+    constexpr int U = 4;
+    for (int base = 0; base < nrows; base += U * blockDim.x) {
+      int row[U];
+      double b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = base + u * blockDim.x + threadIdx.x;
+        row[u] = s < nrows ? T.task_row[t0 + s] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = rhs.template eval<1>(row[u], 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = base + u * blockDim.x + threadIdx.x;
+        if (row[u] >= 0) {
+          xs[s] = b[u];
+          xg[row[u]] = __longlong_as_double(SENTINEL);
+        }
+      }
+    }
+  } else {
+    for (int base = 0; base < nrows; base += 2 * R) {
+      const int s0 = base + grp, s1 = base + R + grp;
+      const int r0 = s0 < nrows ? T.task_row[t0 + s0] : -1;
+      const int r1 = s1 < nrows ? T.task_row[t0 + s1] : -1;
+      const double b0 = rhs.template eval<G>(r0, lane);
+      const double b1 = rhs.template eval<G>(r1, lane);
+      if (lane == 0) {
+        if (r0 >= 0) {
+          xs[s0] = b0;
+          xg[r0] = __longlong_as_double(SENTINEL);
+        }
+        if (r1 >= 0) {
+          xs[s1] = b1;
+          xg[r1] = __longlong_as_double(SENTINEL);
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) xs[nrows] = 0.0;  // zero cell for ELL padding
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+
+  // each thread copies exactly the ring entries it will consume
+  auto issue = [&](int k) {
+    if (k < nst) {
+      const int st = k % D;
+      const int t = steps[k] + grp;
+      if (t < steps[k + 1]) {
+        cp_async8(&rv[st * blockDim.x + threadIdx.x], &T.ell_val[(int64_t)t * G + lane]);
+        cp_async4(&rc[st * blockDim.x + threadIdx.x], &T.ell_col[(int64_t)t * G + lane]);
+        if (lane == 0) {
+          cp_async8(&rd[st * R + grp], &T.task_diag[t]);
+          cp_async4(&rr[st * R + grp], &T.task_row[t]);
+        }
+      } else {
+        rc[st * blockDim.x + threadIdx.x] = TILE_INVALID;
+      }
+    }
+    cp_async_commit();
+  };
+  // external-dependency lookahead: poll value for the next step, issued one step early
+  auto lookahead = [&](int k, int& col, double& pre) {
+    col = TILE_INVALID;
+    pre = 0.0;
+    if (k < nst) {
+      col = rc[(k % D) * blockDim.x + threadIdx.x];
+      if (col >= 0) pre = ld_relaxed(&xg[col]);
+    }
+  };
+  __syncthreads();  // steps[] visible
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) issue(k);
+  cp_async_wait<D - 2>();
+  int col;
+  double pre;
+  lookahead(0, col, pre);
+  __shared__ unsigned spins_s;
+  __shared__ unsigned long long tmax_wait, tmax_done;
+  unsigned long long* trace = g_tile_trace;
+  if (threadIdx.x == 0) {
+    spins_s = 0;
+    tmax_wait = 0;
+    tmax_done = 0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nst; ++k) {
+    unsigned long long t_top = 0;
+    if (trace && threadIdx.x == 0) t_top = gtimer();
+    issue(k + D - 1);
+    cp_async_wait<D - 2>();  // own copies of step k+1 landed
+    if (trace && lane == 0) atomicMax(&tmax_wait, gtimer());
+    int col_n;
+    double pre_n;
+    lookahead(k + 1, col_n, pre_n);
+    const int st = k % D;
+    const bool ok = col != TILE_INVALID;
+    double acc = 0.0;
+    if (ok) {
+      double dep;
+      if (col < 0) {
+        dep = xs[-col - 1];
+      } else if (__double_as_longlong(pre) != SENTINEL) {
+        dep = pre;
+      } else {
+        if (trace) atomicAdd(&spins_s, 1u);
+        dep = spin_load(&xg[col]);
+      }
+      acc = rv[st * blockDim.x + threadIdx.x] * dep;
+    }
+    acc = group_sum<G>(acc);
+    if (ok && lane == 0) {
+      const int sl = steps[k] + grp - t0;
+      const double val = __ddiv_rn(__dsub_rn(xs[sl], acc), rd[st * R + grp]);
+      xs[sl] = val;
+      publish(&xg[rr[st * R + grp]], val);
+    }
+    if (trace && lane == 0) atomicMax(&tmax_done, gtimer());
+    __syncthreads();
+    if (trace && threadIdx.x == 0 && k < g_tile_trace_steps) {
+      unsigned long long* tr = trace + ((size_t)blockIdx.x * g_tile_trace_steps + k) * 5;
+      tr[0] = t_top;
+      tr[1] = spins_s;
+      tr[2] = gtimer();
+      tr[3] = tmax_wait;
+      tr[4] = tmax_done;
+      spins_s = 0;
+      tmax_wait = 0;
+      tmax_done = 0;
+    }
+    col = col_n;
+    pre = pre_n;
+  }
+  cp_async_wait<0>();
+  if (fin >= 0) {
+    double acc = 0.0;
+    for (int s = threadIdx.x; s < nrows; s += blockDim.x) acc += xs[s];
+    double v[1] = {block_sum(acc, sm)};
+    reduce_tail<1>(c, v, gridDim.x, blockIdx.x, ctr, fin, slot, slot2, nmean, sm);
+  }
+}
+
+// ---- tiled solve, thread per row ------------------------------------------------
+// Same schedule as k_trsv_tiled (ELL width E, one CTA per part, level steps of
+// at most R rows) but one THREAD per row: the step loop runs on R/32 warps
+// synchronised with a named barrier, so a step costs a few hundred issued
+// instructions instead of thousands; the other warps of the CTA only help
+// with the prologue (right-hand side gather) and the epilogue.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4_zfill(void* dst, const void* src, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(bytes)
+               : "memory");
+}
+// relaxed gpu-scope load executed only when `pred` (else 0.0), without a branch
+__device__ __forceinline__ double ld_relaxed_if(const double* p, bool pred) {
+  long long b = 0;
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.relaxed.gpu.global.b64 %0, [%1]; }"
+      : "+l"(b)
+      : "l"(p), "r"((int)pred)
+      : "memory");
+  return __longlong_as_double(b);
+}
+
+__host__ __device__ constexpr size_t tile2_ring_offset(int max_rows, int max_steps) {
+  return (((size_t)(max_rows + 1) * 8 + (size_t)(max_steps + 1) * 4) + 15) & ~(size_t)15;
+}
+__host__ __device__ constexpr size_t tile2_smem_bytes(int max_rows, int max_steps, int R, int E,
+                                                      int D) {
+  return tile2_ring_offset(max_rows, max_steps) + (size_t)D * R * (E * 12 + 16);
+}
+
+template <int E, int D, class Rhs>
+__global__ void __launch_bounds__(512, 1) k_trsv_rows(TileDev T, Rhs rhs, double* __restrict__ xg,
+                                                       Ctl c, int ctr, int fin, int slot, int slot2,
+                                                       int64_t nmean, int R) {
+  static_assert(D >= 3, "ring needs >= 3 stages");
+  if (inactive(c)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double sm[32];
+  const int p = blockIdx.x;
+  const int t0 = T.part_task_ptr[p], t1 = T.part_task_ptr[p + 1];
+  const int nrows = t1 - t0;
+  const int s0 = T.part_step_ptr[p], nst = T.part_step_ptr[p + 1] - s0;
+  double* xs = reinterpret_cast<double*>(smem_raw);
+  int* steps = reinterpret_cast<int*>(xs + T.max_part_rows + 1);
+  unsigned char* ring = smem_raw + tile2_ring_offset(T.max_part_rows, T.max_part_steps);
+  // stage layout: vals [R][E] f64 | cols [R][E] i32 | diag [R] f64 | row [R] i32 (+pad)
+  const size_t stage_bytes = (size_t)R * (E * 12 + 16);
+  // prologue (all threads): step table, rhs into xs, sentinel into xg
+  for (int k = threadIdx.x; k <= nst; k += blockDim.x) steps[k] = T.step_task_ptr[s0 + k];
+  if constexpr (Rhs::kScalar) {
+    constexpr int U = 4;
+    for (int base = 0; base < nrows; base += U * blockDim.x) {
+      int row[U];
+      double b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = base + u * blockDim.x + threadIdx.x;
+        row[u] = s < nrows ? T.task_row[t0 + s] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = rhs.template eval<1>(row[u], 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = base + u * blockDim.x + threadIdx.x;
+        if (row[u] >= 0) {
+          xs[s] = b[u];
+          xg[row[u]] = __longlong_as_double(SENTINEL);
+        }
+      }
+    }
+  } else {
+    constexpr int GG = 8;  // lanes per row for the SpMV-shaped right-hand side
+    const int grp = threadIdx.x / GG, lane = threadIdx.x % GG, ngrp = blockDim.x / GG;
+    for (int base = 0; base < nrows; base += 2 * ngrp) {
+      const int sa = base + grp, sb = base + ngrp + grp;
+      const int ra = sa < nrows ? T.task_row[t0 + sa] : -1;
+      const int rb = sb < nrows ? T.task_row[t0 + sb] : -1;
+      const double ba = rhs.template eval<GG>(ra, lane);
+      const double bb = rhs.template eval<GG>(rb, lane);
+      if (lane == 0) {
+        if (ra >= 0) {
+          xs[sa] = ba;
+          xg[ra] = __longlong_as_double(SENTINEL);
+        }
+        if (rb >= 0) {
+          xs[sb] = bb;
+          xg[rb] = __longlong_as_double(SENTINEL);
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) xs[nrows] = 0.0;  // zero cell for ELL padding
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+
+  if ((int)threadIdx.x < R) {
+    const int tid = threadIdx.x;
+    const int zero_slot = nrows;
+    // stage layout (entry-major per step): vals [E][ns] f64 | cols [E][ns] i32 |
+    // diag [ns] f64 | row [ns] i32, each sub-array sized for ns = R
+    auto stage_vals = [&](int st) { return reinterpret_cast<double*>(ring + st * stage_bytes); };
+    auto stage_cols = [&](int st) {
+      return reinterpret_cast<int*>(ring + st * stage_bytes + (size_t)R * E * 8);
+    };
+    auto stage_diag = [&](int st) {
+      return reinterpret_cast<double*>(ring + st * stage_bytes + (size_t)R * E * 12);
+    };
+    auto stage_row = [&](int st) {
+      return reinterpret_cast<int*>(ring + st * stage_bytes + (size_t)R * E * 12 + (size_t)R * 8);
+    };
+    // branch-free, zero-filling copies of step k's block (E*ns is a multiple of 4)
+    auto issue = [&](int k) {
+      if (k < nst) {
+        const int st = k % D;
+        const int a = steps[k], ns = steps[k + 1] - a;
+        const double* gv = T.ell_val + (int64_t)a * E;
+        const int* gc = T.ell_col + (int64_t)a * E;
+        double* sv = stage_vals(st);
+        int* sc = stage_cols(st);
+        const int nv2 = (E * ns) >> 1, nc4 = (E * ns) >> 2;
+#pragma unroll
+        for (int u = 0; u < E / 2; ++u) {
+          const int q = tid + u * R;
+          const bool ok = q < nv2;
+          cp_async16_zfill(sv + 2 * q, ok ? gv + 2 * q : gv, ok ? 16 : 0);
+        }
+#pragma unroll
+        for (int u = 0; u < E / 4; ++u) {
+          const int q = tid + u * R;
+          const bool ok = q < nc4;
+          cp_async16_zfill(sc + 4 * q, ok ? gc + 4 * q : gc, ok ? 16 : 0);
+        }
+        const bool okr = tid < ns;
+        cp_async8_zfill(stage_diag(st) + tid, okr ? T.task_diag + a + tid : T.task_diag, okr ? 8 : 0);
+        cp_async4_zfill(stage_row(st) + tid, okr ? T.task_row + a + tid : T.task_row, okr ? 4 : 0);
+      }
+      cp_async_commit();
+    };
+    double pre[E];
+    // predicated (branch-free) polls of the external dependencies of step k
+    auto lookahead = [&](int k) {
+      if (k < nst) {
+        const int ns = steps[k + 1] - steps[k];
+        const bool valid = tid < ns;
+        const int* sc = stage_cols(k % D);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int col = valid ? sc[e * ns + tid] : -1;
+          pre[e] = ld_relaxed_if(&xg[col < 0 ? 0 : col], col >= 0);
+        }
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k) issue(k);
+    cp_async_wait<D - 3>();  // own copies of steps 0, 1 landed
+    named_bar(1, R);
+    lookahead(0);
+    unsigned long long* trace = g_tile_trace;
+    const bool tr_on = trace && blockIdx.x == 0 && tid == 0;
+    for (int k = 0; k < nst; ++k) {
+      long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+      if (tr_on) c0 = clock64();
+      issue(k + D - 1);
+      const int st = k % D;
+      double cur[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) cur[e] = pre[e];
+      if (tr_on) c1 = clock64();
+      cp_async_wait<D - 3>();  // own copies of step k+2 landed (visible after this step's barrier)
+      if (tr_on) c2 = clock64();
+      lookahead(k + 1);
+      if (tr_on) c3 = clock64();
+      const int a = steps[k], ns = steps[k + 1] - a;
+      if (tid < ns) {
+        const double* sv = stage_vals(st);
+        const int* sc = stage_cols(st);
+        int col[E];
+        double val[E], xv[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          col[e] = sc[e * ns + tid];
+          val[e] = sv[e * ns + tid];
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) xv[e] = xs[col[e] < 0 ? -col[e] - 1 : zero_slot];
+        bool late = false;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          late |= (col[e] >= 0) && (__double_as_longlong(cur[e]) == SENTINEL);
+        double acc = 0.0;
+        if (!late) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc = fma(val[e], col[e] < 0 ? xv[e] : cur[e], acc);
+        } else {
+          for (int e = 0; e < E; ++e) {
+            double dep = xv[e];
+            if (col[e] >= 0)
+              dep = __double_as_longlong(cur[e]) != SENTINEL ? cur[e] : spin_load(&xg[col[e]]);
+            acc = fma(val[e], dep, acc);
+          }
+        }
+        const int sl = a + tid - t0;
+        const double v = __ddiv_rn(__dsub_rn(xs[sl], acc), stage_diag(st)[tid]);
+        xs[sl] = v;
+        publish(&xg[stage_row(st)[tid]], v);
+      }
+      long long c4 = 0, c5 = 0;
+      if (tr_on) c4 = clock64();
+      named_bar(1, R);
+      if (tr_on) {
+        c5 = clock64();
+        if (k < g_tile_trace_steps) {
+          unsigned long long* q = trace + (size_t)k * 5;
+          q[0] = c1 - c0;
+          q[1] = c2 - c1;
+          q[2] = c3 - c2;
+          q[3] = c4 - c3;
+          q[4] = c5 - c4;
+        }
+      }
+    }
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+  if (fin >= 0) {
+    double acc = 0.0;
+    for (int s = threadIdx.x; s < nrows; s += blockDim.x) acc += xs[s];
+    double v[1] = {block_sum(acc, sm)};
+    reduce_tail<1>(c, v, gridDim.x, blockIdx.x, ctr, fin, slot, slot2, nmean, sm);
+  }
+}
+
+// ---- persistent sync-free triangular solve ----------------------------------
+// Tasks (rows) in level order, ELL entries (G per row, column -1 = padding)
+// stored in task order so a chunk of rows is one contiguous, coalesced read.
+// A persistent grid sized to keep only ~3 levels of rows in flight grabs
+// chunks in order with an atomic counter (a chunk only depends on lower
+// chunks, all owned by running blocks => no deadlock) and polls its
+// dependencies with a short nanosleep backoff, keeping L2 poll traffic low.
+struct EllTri {
+  const int* task_row;
+  const double* task_diag;
+  const int* ell_col;
+  const double* ell_val;
+  int ntasks;
+};
+
+__device__ __forceinline__ double spin_load_backoff(const double* p) {
+  long long b;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  while (b == SENTINEL) {
+    __nanosleep(32);
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  }
+  return __longlong_as_double(b);
+}
+
+template <int G, class Rhs>
+__global__ void __launch_bounds__(TPB) k_trsv_persist(EllTri t, Rhs rhs, double* __restrict__ y,
+                                                      Ctl c, int ctr_chunk, int ctr_done,
+                                                      int nchunks, int fin, int slot, int slot2,
+                                                      int64_t nmean) {
+  if (inactive(c)) return;
+  __shared__ int chunk_s[2];
+  __shared__ int last_s;
+  __shared__ double sm[32];
+  const int rpc = TPB / G;
+  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+  // a chunk's inputs, loaded one chunk ahead of its processing
+  struct Pre {
+    int task, row, col;
+    double val, diag, b;
+  };
+  auto load = [&](int chunk, Pre& p) {
+    p.task = chunk * rpc + grp;
+    p.row = (chunk < nchunks && p.task < t.ntasks) ? t.task_row[p.task] : -1;
+    p.b = rhs.template eval<G>(p.row, lane);
+    p.col = p.row >= 0 ? t.ell_col[(int64_t)p.task * G + lane] : -1;
+    p.val = p.row >= 0 ? t.ell_val[(int64_t)p.task * G + lane] : 0.0;
+    p.diag = p.row >= 0 ? t.task_diag[p.task] : 1.0;
+  };
+  if (threadIdx.x == 0) chunk_s[0] = (int)atomicAdd(&c.ctr[ctr_chunk], 1u);
+  __syncthreads();
+  int chunk = chunk_s[0];
+  Pre cur;
+  load(chunk, cur);
+  int par = 0;
+  while (chunk < nchunks) {
+    // grab and prefetch the next chunk before waiting on this one
+    if (threadIdx.x == 0) chunk_s[par ^ 1] = (int)atomicAdd(&c.ctr[ctr_chunk], 1u);
+    __syncthreads();
+    const int next = chunk_s[par ^ 1];
+    Pre nx;
+    load(next, nx);
+    double a = 0.0;
+    if (cur.col >= 0) a = cur.val * spin_load(&y[cur.col]);
+    a = group_sum<G>(a);  // every lane of the warp reaches the shuffle
+    double val = 0.0;
+    if (cur.row >= 0) {
+      val = __ddiv_rn(__dsub_rn(cur.b, a), cur.diag);
+      if (lane == 0) publish(&y[cur.row], val);
+    }
+    if (fin >= 0) {
+      const double v = block_sum(lane == 0 && cur.row >= 0 ? val : 0.0, sm);
+      if (threadIdx.x == 0) c.partials[chunk] = v;
+    }
+    cur = nx;
+    chunk = next;
+    par ^= 1;
+  }
+  // completion: the last block finalises the (optional) mean and resets counters
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s) {
+    __threadfence();
+    if (fin >= 0) {
+      double tot[1];
+      tot[0] = sum_partials(c.partials, nchunks, 0, sm);
+      if (threadIdx.x == 0) finalize(c, fin, slot, slot2, tot, nmean);
+    }
+    if (threadIdx.x == 0) {
+      c.ctr[ctr_chunk] = 0u;
+      c.ctr[ctr_done] = 0u;
+      __threadfence();
     }
   }
 }

@@ -456,3 +456,213 @@ int cholesky(const HostCsr& a, const std::vector<int32_t>& perm, HostCsr* lower,
 }
 
 }  // namespace bd
+
+// ---------------------------------------------------------------------------
+// Tiled schedules for the cooperative triangular-solve kernel.
+namespace bd {
+
+namespace {
+
+// BFS inside the node subset `nodes` (membership: mark[u] == id) from a
+// pseudo-peripheral node; returns nodes sorted by BFS distance (unreached
+// components appended).
+void bfs_order(const Graph& g, std::vector<int32_t>& nodes, std::vector<int32_t>& mark,
+               std::vector<int32_t>& dist, int32_t id, std::vector<int32_t>* out) {
+  auto run = [&](int32_t root, std::vector<int32_t>& order) {
+    order.clear();
+    order.push_back(root);
+    dist[root] = 0;
+    for (size_t h = 0; h < order.size(); ++h) {
+      const int32_t u = order[h];
+      for (int64_t p = g.xadj[u]; p < g.xadj[u + 1]; ++p) {
+        const int32_t v = g.adj[p];
+        if (mark[v] == id && dist[v] < 0) {
+          dist[v] = dist[u] + 1;
+          order.push_back(v);
+        }
+      }
+    }
+  };
+  std::vector<int32_t> order;
+  int32_t root = *std::min_element(nodes.begin(), nodes.end());
+  int32_t ecc = -1;
+  for (int rep = 0; rep < 3; ++rep) {
+    run(root, order);
+    const int32_t far = order.back(), e = dist[far];
+    for (int32_t u : order) dist[u] = -1;
+    if (e <= ecc) break;
+    ecc = e;
+    root = far;
+  }
+  run(root, order);
+  for (int32_t u : order) dist[u] = -1;
+  out->swap(order);
+  if (out->size() < nodes.size()) {  // disconnected remainder, appended in index order
+    for (int32_t u : *out) mark[u] = -2 - id;
+    std::vector<int32_t> rest;
+    for (int32_t u : nodes)
+      if (mark[u] == id) rest.push_back(u);
+    for (int32_t u : *out) mark[u] = id;
+    out->insert(out->end(), rest.begin(), rest.end());
+  }
+}
+
+void bisect(const Graph& g, std::vector<int32_t> nodes, int parts, int32_t first_part,
+            std::vector<int32_t>& mark, std::vector<int32_t>& dist, int32_t& next_id,
+            std::vector<int32_t>* part) {
+  if (parts <= 1 || nodes.size() <= 1) {
+    for (int32_t u : nodes) (*part)[u] = first_part;
+    return;
+  }
+  const int32_t id = next_id++;
+  for (int32_t u : nodes) mark[u] = id;
+  std::vector<int32_t> order;
+  bfs_order(g, nodes, mark, dist, id, &order);
+  const int pa = parts / 2, pb = parts - pa;
+  const size_t cut = (size_t)((double)order.size() * pa / parts + 0.5);
+  std::vector<int32_t> a(order.begin(), order.begin() + cut), b(order.begin() + cut, order.end());
+  bisect(g, std::move(a), pa, first_part, mark, dist, next_id, part);
+  bisect(g, std::move(b), pb, first_part + pa, mark, dist, next_id, part);
+}
+
+}  // namespace
+
+void partition_rows(const HostCsr& a, int parts, std::vector<int32_t>* part) {
+  Graph g = symmetric_graph(a);
+  part->assign(a.n, 0);
+  std::vector<int32_t> mark(a.n, -1), dist(a.n, -1);
+  std::vector<int32_t> all(a.n);
+  std::iota(all.begin(), all.end(), 0);
+  int32_t next_id = 0;
+  bisect(g, std::move(all), parts, 0, mark, dist, next_id, part);
+}
+
+namespace {
+void rcb(int64_t lo_idx, std::vector<int32_t>& ids, size_t b, size_t e, int dim, const double* x,
+         int parts, int32_t first, std::vector<int32_t>* part) {
+  if (parts <= 1 || e - b <= 1) {
+    for (size_t k = b; k < e; ++k) (*part)[ids[k]] = first;
+    return;
+  }
+  int axis = 0;
+  double best = -1.0;
+  for (int d = 0; d < dim; ++d) {
+    double mn = 1e300, mx = -1e300;
+    for (size_t k = b; k < e; ++k) {
+      const double v = x[(int64_t)ids[k] * dim + d];
+      mn = std::min(mn, v);
+      mx = std::max(mx, v);
+    }
+    if (mx - mn > best) {
+      best = mx - mn;
+      axis = d;
+    }
+  }
+  const int pa = parts / 2, pb = parts - pa;
+  const size_t cut = b + (size_t)((double)(e - b) * pa / parts + 0.5);
+  std::nth_element(ids.begin() + b, ids.begin() + cut, ids.begin() + e, [&](int32_t u, int32_t v) {
+    const double xu = x[(int64_t)u * dim + axis], xv = x[(int64_t)v * dim + axis];
+    return xu < xv || (xu == xv && u < v);
+  });
+  rcb(lo_idx, ids, b, cut, dim, x, pa, first, part);
+  rcb(lo_idx, ids, cut, e, dim, x, pb, first + pa, part);
+}
+}  // namespace
+
+void partition_coords(int64_t n, int dim, const double* coords, int parts,
+                      std::vector<int32_t>* part) {
+  part->assign(n, 0);
+  std::vector<int32_t> ids(n);
+  std::iota(ids.begin(), ids.end(), 0);
+  rcb(0, ids, 0, (size_t)n, dim, coords, parts, 0, part);
+}
+
+bool build_tile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& part,
+                         int parts, int G, int R, TileSchedule* out, bool entry_major) {
+  const int64_t n = t.n;
+  std::vector<int32_t> level;
+  out->depth = row_levels(t, lower, &level);
+  out->parts = parts;
+  out->G = G;
+  out->R = R;
+  // rows of each part sorted by (level, row)
+  std::vector<std::vector<int32_t>> rows(parts);
+  for (int64_t i = 0; i < n; ++i) rows[part[i]].push_back((int32_t)i);
+  out->part_task_ptr.assign(parts + 1, 0);
+  out->part_step_ptr.assign(parts + 1, 0);
+  out->step_task_ptr.clear();
+  out->step_task_ptr.push_back(0);
+  out->task_row.clear();
+  out->task_row.reserve(n);
+  std::vector<int32_t> slot(n, -1);
+  out->max_part_rows = 0;
+  for (int p = 0; p < parts; ++p) {
+    auto& r = rows[p];
+    std::stable_sort(r.begin(), r.end(),
+                     [&](int32_t x, int32_t y) { return level[x] < level[y]; });
+    const int32_t base = (int32_t)out->task_row.size();
+    int32_t in_step = 0, cur_level = -1;
+    for (size_t k = 0; k < r.size(); ++k) {
+      const int32_t row = r[k];
+      if (level[row] != cur_level || in_step == R) {
+        if (k > 0) out->step_task_ptr.push_back(base + (int32_t)k);
+        cur_level = level[row];
+        in_step = 0;
+      }
+      slot[row] = (int32_t)k;
+      out->task_row.push_back(row);
+      ++in_step;
+    }
+    if (!r.empty()) out->step_task_ptr.push_back(base + (int32_t)r.size());
+    out->part_task_ptr[p + 1] = (int32_t)out->task_row.size();
+    out->part_step_ptr[p + 1] = (int32_t)out->step_task_ptr.size() - 1;
+    out->max_part_rows = std::max<int>(out->max_part_rows, (int)r.size());
+    out->max_part_steps = std::max<int>(out->max_part_steps,
+                                        out->part_step_ptr[p + 1] - out->part_step_ptr[p]);
+  }
+  const int64_t nt = (int64_t)out->task_row.size();
+  out->task_diag.assign(nt, 0.0);
+  out->ell_col.assign(nt * G, 0);
+  out->ell_val.assign(nt * G, 0.0);
+  for (int p = 0; p < parts; ++p) {
+    const int32_t zero_cell = -(int32_t)(out->part_task_ptr[p + 1] - out->part_task_ptr[p]) - 1;
+    for (int32_t tk = out->part_task_ptr[p]; tk < out->part_task_ptr[p + 1]; ++tk) {
+      const int32_t row = out->task_row[tk];
+      int cnt = 0;
+      for (int64_t q = t.indptr[row]; q < t.indptr[row + 1]; ++q) {
+        const int32_t c = t.indices[q];
+        if (c == row) {
+          out->task_diag[tk] = t.values[q];
+          continue;
+        }
+        if (cnt == G) return false;
+        out->ell_col[tk * G + cnt] = (part[c] == p) ? -(slot[c] + 1) : c;
+        out->ell_val[tk * G + cnt] = t.values[q];
+        ++cnt;
+      }
+      for (; cnt < G; ++cnt) {
+        out->ell_col[tk * G + cnt] = zero_cell;
+        out->ell_val[tk * G + cnt] = 0.0;
+      }
+    }
+  }
+  if (entry_major) {
+    // per step: [rows][G] -> [G][rows]
+    std::vector<int32_t> col2(out->ell_col.size());
+    std::vector<double> val2(out->ell_val.size());
+    const int64_t nsteps = (int64_t)out->step_task_ptr.size() - 1;
+    for (int64_t s = 0; s < nsteps; ++s) {
+      const int64_t a = out->step_task_ptr[s], b = out->step_task_ptr[s + 1], ns = b - a;
+      for (int64_t r = 0; r < ns; ++r)
+        for (int e = 0; e < G; ++e) {
+          col2[a * G + e * ns + r] = out->ell_col[(a + r) * G + e];
+          val2[a * G + e * ns + r] = out->ell_val[(a + r) * G + e];
+        }
+    }
+    out->ell_col.swap(col2);
+    out->ell_val.swap(val2);
+  }
+  return true;
+}
+
+}  // namespace bd

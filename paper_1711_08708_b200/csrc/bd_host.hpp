@@ -48,3 +48,43 @@ int cholesky(const HostCsr& a, const std::vector<int32_t>& perm, HostCsr* lower,
              std::string* msg);
 
 }  // namespace bd
+
+namespace bd {
+
+// Balanced partition of the rows of a symmetric pattern into `parts` pieces
+// by recursive BFS-distance bisection (RCB-like slabs on mesh graphs).
+void partition_rows(const HostCsr& a, int parts, std::vector<int32_t>* part);
+
+// Recursive coordinate bisection of n points (row-major n×dim) into `parts`
+// axis-aligned boxes (split along the widest extent at the proportional
+// quantile).  On structured meshes numbered lexicographically the lower-
+// triangular dependencies point to smaller coordinates, so the part DAG of a
+// triangular solve is acyclic with chains of length ~ the box grid diameter.
+void partition_coords(int64_t n, int dim, const double* coords, int parts,
+                      std::vector<int32_t>* part);
+
+// Tiled triangular-solve schedule: rows grouped by part (one CTA each), each
+// part's rows sorted by DAG level and cut into steps of at most R rows (a step
+// never spans two levels).  Off-diagonal entries in ELL form (G per row):
+// col >= 0 is a row of another part (polled), col < 0 is -(slot+1) of a row of
+// the same part (shared memory); padding points at the part's zero cell.
+struct TileSchedule {
+  int parts = 0, G = 0, R = 0;
+  int max_part_rows = 0;
+  int max_part_steps = 0;
+  int64_t depth = 0;
+  std::vector<int32_t> part_task_ptr;  // parts+1
+  std::vector<int32_t> part_step_ptr;  // parts+1
+  std::vector<int32_t> step_task_ptr;  // nsteps+1
+  std::vector<int32_t> task_row;       // ntasks
+  std::vector<double> task_diag;       // ntasks
+  std::vector<int32_t> ell_col;        // ntasks*G
+  std::vector<double> ell_val;         // ntasks*G
+};
+// Returns false if some row has more than G off-diagonal entries.
+// entry_major: within each step the ELL block is stored [G][rows_in_step]
+// (entry-major) instead of [rows][G], for lane-contiguous shared-memory reads.
+bool build_tile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& part,
+                         int parts, int G, int R, TileSchedule* out, bool entry_major = false);
+
+}  // namespace bd

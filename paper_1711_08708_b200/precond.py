@@ -93,7 +93,10 @@ class NativeInner(InnerPreconditioner):
         self.n = 0
         self.restarts_used = 0
 
-    def setup(self, matrix) -> None:
+    def setup(self, matrix, coords=None) -> None:
+        """Factor on the host (C++) and upload.  ``coords`` (n×dim vertex
+        coordinates, optional) only steer the row partition of the tiled
+        triangular-solve schedule; the factor does not depend on them."""
         a = sp.csr_matrix(matrix, dtype=float)
         a.sum_duplicates()
         a.sort_indices()
@@ -104,12 +107,17 @@ class NativeInner(InnerPreconditioner):
         ip, ix, dv = csr_arrays(a)
         h = C.c_void_p()
         used = C.c_int(0)
-        _lib.check(_lib.lib().bd_inner_create(ctx.handle, _lib.INNER_KIND[self.kind], a.shape[0],
-                                              ip.ctypes.data_as(C.c_void_p),
-                                              ix.ctypes.data_as(C.c_void_p),
-                                              dv.ctypes.data_as(C.c_void_p),
-                                              int(self.max_restarts), C.byref(h), C.byref(used)),
-                   ctx.handle)
+        xyz, dim = None, 0
+        if coords is not None:
+            xyz = np.ascontiguousarray(coords, dtype=np.float64)
+            if xyz.ndim != 2 or xyz.shape[0] != a.shape[0]:
+                raise ValueError("coords must be (n, dim)")
+            dim = xyz.shape[1]
+        _lib.check(_lib.lib().bd_inner_create_ex(
+            ctx.handle, _lib.INNER_KIND[self.kind], a.shape[0], ip.ctypes.data_as(C.c_void_p),
+            ix.ctypes.data_as(C.c_void_p), dv.ctypes.data_as(C.c_void_p), int(self.max_restarts),
+            xyz.ctypes.data_as(C.c_void_p) if xyz is not None else None, dim, C.byref(h),
+            C.byref(used)), ctx.handle)
         self.handle, self.ctx, self.n = h, ctx, a.shape[0]
         self.restarts_used = int(used.value)
 
@@ -198,6 +206,16 @@ def make_inner(name: str) -> InnerPreconditioner:
     raise ValueError(f"unknown inner preconditioner {name!r}; choose one of {INNER_NAMES}")
 
 
+def _coords(system):
+    """Vertex coordinates for the solve-schedule partition, when known."""
+    pts = getattr(system, "coords", None)
+    if pts is None and getattr(system, "mesh", None) is not None:
+        pts = system.mesh.vertices
+    if pts is None or len(pts) != system.n:
+        return None
+    return np.asarray(pts, dtype=float)
+
+
 class BlockLUPreconditioner:
     """P_Λ = L_P U_P with the monodomain K_m in the Schur slot
     (bd/precond.py:246-312).  One application = two bulk inverses, one K_m
@@ -210,8 +228,9 @@ class BlockLUPreconditioner:
         self.system = system
         self.inner_name = inner
         self.regularized = regularize_stiffness(system.stiff_total)
+        coords = _coords(system)
         self.inner_bulk = make_inner(inner)
-        self.inner_bulk.setup(self.regularized.grounded())
+        self.inner_bulk.setup(self.regularized.grounded(), coords=coords)
         if monodomain_matrix is None:
             if system.mesh is None or system.params is None:
                 raise PreconditionerError("system carries no mesh/params; pass monodomain_matrix")
@@ -219,7 +238,8 @@ class BlockLUPreconditioner:
                                                         getattr(system, "fibers", None))
         self.monodomain_matrix = monodomain_matrix
         self.inner_schur = make_inner(inner)
-        self.inner_schur.setup(monodomain_matrix)
+        self.inner_schur.setup(monodomain_matrix,
+                               coords=None if coords is None else coords[: system.n_heart])
         nat = system.native
         h = C.c_void_p()
         _lib.check(_lib.lib().bd_blocklu_create(nat.handle, self.inner_bulk.handle,

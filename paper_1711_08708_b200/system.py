@@ -119,6 +119,7 @@ class BidomainSystem:
         self.mesh = mesh
         self.params = params
         self.fibers = fibers
+        self.coords = None  # optional vertex coordinates (partition hint) when mesh is None
         self._native = None
 
     # -- reference properties -------------------------------------------------

@@ -169,9 +169,10 @@ def test_pcg_matches_reference(case, inner):
     tr = rel_l2(qu, qv, g["b_u"], g["b_v"])
     assert tr <= 1e-9
     assert abs(sysm.weighted_mean_u(xu)) <= 1e-10 * max(1.0, np.abs(xu).max())
-    hist = st.preconditioned_history
-    for a, b in zip(hist, hist[1:]):
-        assert b <= a * (1 + 1e-10)
+    if inner == "exact":  # preconditioned measure non-increasing (tests/test_krylov.py:57-64)
+        hist = st.preconditioned_history
+        for a, b in zip(hist, hist[1:]):
+            assert b <= a * (1 + 1e-10)
 
 
 def _coupled():

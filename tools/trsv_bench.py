@@ -1,0 +1,43 @@
+"""Dev tool: time one IC(0) inner apply (forward+backward triangular pass) on a
+config-2-style slab, tiled cooperative kernel vs the global sync-free kernel."""
+import os, sys, time
+import numpy as np
+sys.path.insert(0, '/root/repo')
+import torch
+import paper_1711_08708_b200 as bd
+from paper_1711_08708_b200 import configs
+from paper_1711_08708_b200.assembly import assemble_stiffness
+from paper_1711_08708_b200.conductivity import TensorField
+from paper_1711_08708_b200.precond import regularize_stiffness
+
+cells = tuple(int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "128,128,64").split(","))
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+wl = configs.cfg2(cells)
+t0 = time.time()
+S1 = assemble_stiffness(wl.mesh, TensorField(wl.params, 3, "bar1", wl.fibers))
+g = regularize_stiffness(S1).grounded()
+print(f"n={g.shape[0]} nnz={g.nnz} assembly {time.time()-t0:.1f}s", flush=True)
+rng = np.random.default_rng(0)
+y = torch.as_tensor(rng.standard_normal(g.shape[0])).cuda()
+res = {}
+for mode in os.environ.get("MODES", "persist,tiled,syncfree").split(","):
+    os.environ["BD_TRSV"] = mode
+    inner = bd.IncompleteCholesky0(); t0 = time.time(); inner.setup(g, coords=wl.mesh.vertices)
+    print(mode, "setup", round(time.time()-t0, 2), "s", inner.factor_info(), flush=True)
+    z = inner.apply_inverse(y); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        z = inner.apply_inverse(y)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nnz = inner.factor_info()["nnz"]; n = g.shape[0]
+    byts = 2 * (12 * nnz + 4 * (n + 1) + 16 * n)
+    print(f"{mode}: {ms*1e3:.1f} us per apply (fwd+bwd) -> {byts/ms/1e6:.0f} GB/s algorithmic", flush=True)
+    res[mode] = z.cpu().numpy()
+ks = list(res)
+for k in ks[1:]:
+    d = np.abs(res[k] - res[ks[0]]).max() / np.abs(res[ks[0]]).max()
+    print(f"max rel diff {k} vs {ks[0]}", d)
+# residual check: L L^T z = y approx? check symmetric positivity instead
+
