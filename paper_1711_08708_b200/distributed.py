@@ -1,0 +1,362 @@
+"""Mesh-partitioned (multi-GPU) coupled solve: partition, halo plan, distributed PCG.
+
+One process per GPU.  The vertices are split by recursive coordinate
+bisection (RCB); each rank owns a box of vertices and keeps a one-layer ghost
+halo (P1 stencils only couple mesh neighbours).  Local numbering keeps the
+reference's heart-first property per rank: owned heart vertices, owned torso
+vertices, then ghost heart, ghost torso.  So the local v block is a prefix of
+the local u block, as `bd/mesh.py:252-263` guarantees globally.
+
+The distributed iteration is `pcg_solve` (bd/krylov.py:46-140) with the
+block-LU preconditioner (bd/precond.py:281-312), with two changes:
+* dots and means are global, via all_reduce; Λ and the two S_i products
+  exchange halos;
+* the inner solves become block-Jacobi: the owned diagonal block of the
+  grounded S_1 / K_m.  Jacobi shards exactly; IC(0) and exact change the
+  preconditioner, so their iteration counts are reported next to the
+  1-GPU counts.
+
+Local compute goes through a backend object.  ``NativeBackend`` runs SpMV and
+the inner solves in the sm_100a library.  The CPU tests inject a scipy backend
+(tests/test_distributed.py) to check the partition / halo / collective logic
+with gloo at world size 2.  Vectors are torch tensors on the rank's device;
+collectives are torch.distributed (NCCL over NVLink on the box).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+
+# ---- partition (host) ----------------------------------------------------------
+def rcb_partition(coords: np.ndarray, parts: int) -> np.ndarray:
+    """Recursive coordinate bisection: split along the widest extent at the
+    proportional quantile; returns the part id of every point."""
+    coords = np.asarray(coords, dtype=float)
+    out = np.zeros(coords.shape[0], dtype=np.int64)
+
+    def rec(ids, p, first):
+        if p <= 1 or ids.size <= 1:
+            out[ids] = first
+            return
+        x = coords[ids]
+        axis = int(np.argmax(x.max(axis=0) - x.min(axis=0)))
+        pa = p // 2
+        cut = int(round(ids.size * pa / p))
+        order = np.lexsort((ids, x[:, axis]))
+        rec(ids[order[:cut]], pa, first)
+        rec(ids[order[cut:]], p - pa, first + pa)
+
+    rec(np.arange(coords.shape[0]), parts, 0)
+    return out
+
+
+@dataclass
+class LocalProblem:
+    """Rank-local blocks in local numbering (owned heart, owned torso, ghost
+    heart, ghost torso) and the halo plan."""
+
+    rank: int
+    nprocs: int
+    n_global: int
+    m_global: int
+    owned: np.ndarray          # global ids of owned vertices, local order
+    ghosts: np.ndarray         # global ids of ghost vertices, local order
+    n_own: int
+    m_own: int                 # owned heart vertices (prefix of owned)
+    m_ghost: int               # ghost heart vertices (prefix of ghosts)
+    S1: sp.csr_matrix          # n_own × (n_own + n_ghost)
+    Si: sp.csr_matrix          # m_own × (m_own + m_ghost)
+    mass: np.ndarray           # n_own
+    heart_mass: np.ndarray     # m_own
+    gamma: float
+    bulk_block: sp.csr_matrix  # owned diagonal block of the grounded S_1
+    schur_block: sp.csr_matrix  # owned diagonal block of K_m
+    # halo plan: per neighbour, local indices to send / ghost slots to fill
+    send: dict = field(default_factory=dict)
+    recv: dict = field(default_factory=dict)
+    send_heart: dict = field(default_factory=dict)
+    recv_heart: dict = field(default_factory=dict)
+
+
+def build_local(S1, Si, mass, heart_mass, gamma, grounded, Km, part: np.ndarray,
+                rank: int, nprocs: int) -> LocalProblem:
+    """Rank `rank`'s local problem from the global CSR blocks (every rank can
+    compute every rank's plan: the halo lists are consistent by construction)."""
+    S1 = sp.csr_matrix(S1)
+    Si = sp.csr_matrix(Si)
+    n, m = S1.shape[0], Si.shape[0]
+    part = np.asarray(part)
+
+    def layout(r):
+        own = np.flatnonzero(part == r)
+        own = np.concatenate([own[own < m], own[own >= m]])
+        rows = S1[own]
+        cols = np.unique(rows.indices)
+        gh = cols[part[cols] != r]
+        gh = np.concatenate([gh[gh < m], gh[gh >= m]])
+        return own, gh
+
+    lay = [layout(r) for r in range(nprocs)]
+    owned, ghosts = lay[rank]
+    n_own, m_own = owned.size, int((owned < m).sum())
+    m_ghost = int((ghosts < m).sum())
+    ext = np.concatenate([owned, ghosts])
+    g2l = -np.ones(n, dtype=np.int64)
+    g2l[ext] = np.arange(ext.size)
+    s1 = S1[owned][:, ext]
+    # heart extended numbering: owned heart, ghost heart
+    hext = np.concatenate([owned[:m_own], ghosts[:m_ghost]])
+    si = Si[owned[:m_own]][:, hext]
+    for a in (s1, si):
+        a.sort_indices()
+    gb = sp.csr_matrix(grounded)[owned][:, owned]
+    kb = sp.csr_matrix(Km)[owned[:m_own]][:, owned[:m_own]]
+    lp = LocalProblem(rank, nprocs, n, m, owned, ghosts, n_own, m_own, m_ghost, s1.tocsr(),
+                      si.tocsr(), np.asarray(mass)[owned], np.asarray(heart_mass)[owned[:m_own]],
+                      float(gamma), gb.tocsr(), kb.tocsr())
+    # halo: my ghosts owned by q are received from q in q's send order
+    for q in range(nprocs):
+        if q == rank:
+            continue
+        q_own, q_gh = lay[q]
+        # what q needs from me: q's ghosts that I own, in q's ghost order
+        need_from_me = q_gh[part[q_gh] == rank]
+        if need_from_me.size:
+            lp.send[q] = g2l[need_from_me]
+            hm = need_from_me < m
+            if hm.any():
+                lp.send_heart[q] = g2l[need_from_me[hm]]
+        mine = ghosts[part[ghosts] == q]
+        if mine.size:
+            lp.recv[q] = g2l[mine] - n_own  # ghost slots
+            hm = mine < m
+            if hm.any():
+                # heart ghosts are the prefix of ghosts: slot = ghost index
+                lp.recv_heart[q] = g2l[mine[hm]] - n_own
+    return lp
+
+
+# ---- communication -------------------------------------------------------------------
+class Comm:
+    """torch.distributed wrapper: halo exchange and global sums."""
+
+    def __init__(self, dist, device):
+        self.dist = dist
+        self.device = device
+
+    def allreduce(self, vals):
+        torch = _torch()
+        t = torch.tensor(vals, dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t)
+        return t.tolist()
+
+    def halo(self, x_own, send: dict, recv: dict, nslots: int):
+        """Ghost values of x from the owning neighbours (one layer)."""
+        torch = _torch()
+        out = torch.zeros(nslots, dtype=x_own.dtype, device=x_own.device)
+        ops, bufs = [], {}
+        for q, idx in send.items():
+            buf = x_own[torch.as_tensor(idx, device=x_own.device)].contiguous()
+            ops.append(self.dist.P2POp(self.dist.isend, buf, q))
+        for q, slots in recv.items():
+            bufs[q] = torch.empty(len(slots), dtype=x_own.dtype, device=x_own.device)
+            ops.append(self.dist.P2POp(self.dist.irecv, bufs[q], q))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        for q, slots in recv.items():
+            out[torch.as_tensor(slots, device=x_own.device)] = bufs[q]
+        return out
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---- distributed operator and solver ----------------------------------------------------
+class DistributedSystem:
+    """Λ on the rank's owned rows (block vector = [u_own | v_own])."""
+
+    def __init__(self, lp: LocalProblem, comm: Comm, backend):
+        self.lp, self.comm, self.be = lp, comm, backend
+        self.S1 = backend.matrix(lp.S1)
+        self.Si = backend.matrix(lp.Si)
+        torch = _torch()
+        self.mh = torch.as_tensor(lp.heart_mass, device=comm.device)
+        self.mass = torch.as_tensor(lp.mass, device=comm.device)
+        self.msum = comm.allreduce([float(lp.mass.sum())])[0]
+
+    @property
+    def n(self):
+        return self.lp.n_own
+
+    @property
+    def m(self):
+        return self.lp.m_own
+
+    def ext_u(self, u):
+        lp = self.lp
+        g = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size)
+        return _torch().cat([u, g]), g
+
+    def ext_heart(self, v_own, ghost_heart):
+        return _torch().cat([v_own, ghost_heart])
+
+    def heart_ghosts(self, v):
+        lp = self.lp
+        return self.comm.halo(v, lp.send_heart, lp.recv_heart, lp.m_ghost)
+
+    def apply(self, x):
+        """q = Λ x (bd/system.py:106-116) with halo exchanges of u and v."""
+        lp = self.lp
+        u, v = x[: lp.n_own], x[lp.n_own:]
+        ue, ug = self.ext_u(u)
+        ve = self.ext_heart(v, self.heart_ghosts(v))
+        ue_h = self.ext_heart(u[: lp.m_own], ug[: lp.m_ghost])
+        iv = self.be.spmv(self.Si, ve)
+        iu = self.be.spmv(self.Si, ue_h)
+        top = self.be.spmv(self.S1, ue)
+        top[: lp.m_own] += iv
+        bottom = iu + iv + lp.gamma * (self.mh * v)
+        return _torch().cat([top, bottom])
+
+    def dot(self, a, b):
+        return self.comm.allreduce([float((a * b).sum())])[0]
+
+    def mean_u(self, u):
+        return self.comm.allreduce([float(u.sum())])[0] / self.lp.n_global
+
+    def normalize(self, x):
+        lp = self.lp
+        alpha = self.comm.allreduce([float((self.mass * x[: lp.n_own]).sum())])[0] / self.msum
+        out = x.clone()
+        out[: lp.n_own] -= alpha
+        return out
+
+
+class DistributedBlockLU:
+    """Block-LU P_Λ (bd/precond.py:281-312) with block-Jacobi inner solves."""
+
+    def __init__(self, dsys: DistributedSystem, inner: str, beta: float):
+        self.s, self.beta = dsys, beta
+        be = dsys.be
+        self.bulk = be.inner(inner, dsys.lp.bulk_block)
+        self.schur = be.inner(inner, dsys.lp.schur_block)
+        self.p1 = self.pk = self.si = 0
+
+    def bulk_inverse(self, y):
+        self.p1 += 1
+        s = self.s
+        mean = s.mean_u(y)
+        z = s.be.inner_apply(self.bulk, y - mean)
+        z = z - s.mean_u(z)
+        return z + mean / self.beta
+
+    def apply(self, r):
+        s, lp = self.s, self.s.lp
+        ru, rv = r[: lp.n_own], r[lp.n_own:]
+        t = self.bulk_inverse(ru)
+        th = s.ext_heart(t[: lp.m_own], s.heart_ghosts(t[: lp.m_own]))  # collective on all ranks
+        self.si += 1
+        self.pk += 1
+        sv = s.be.inner_apply(self.schur, rv - s.be.spmv(s.Si, th))
+        sg = s.heart_ghosts(sv)
+        self.si += 1
+        corr = _torch().zeros_like(ru)
+        corr[: lp.m_own] = s.be.spmv(s.Si, s.ext_heart(sv, sg))
+        u = t - self.bulk_inverse(corr)
+        return _torch().cat([u, sv])
+
+
+def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e-6,
+                    max_iter=500, x0=None):
+    """The reference iteration (bd/krylov.py:46-140) on the sharded system.
+    Returns (x_local, stats dict); raises RuntimeError past max_iter / breakdown."""
+    st = {"iterations": 0, "residual_history": [], "preconditioned_history": [],
+          "mv_count": 0, "converged": False}
+    n = dsys.n
+    nb = dsys.dot(b, b) ** 0.5
+    torch = _torch()
+    if nb == 0.0:
+        st["residual_history"].append(0.0)
+        st["converged"] = True
+        return torch.zeros_like(b), st
+    if x0 is None:
+        x = torch.zeros_like(b)
+        r = b.clone()
+    else:
+        x = x0.clone()
+        r = b - dsys.apply(x)
+    st["mv_count"] += 1
+    rel = dsys.dot(r, r) ** 0.5 / nb
+    st["residual_history"].append(rel)
+    if rel <= tol:
+        st["converged"] = True
+        return dsys.normalize(x), st
+
+    def precond(r):
+        z = prec.apply(r)
+        z[:n] -= dsys.mean_u(z[:n])  # _deflate
+        return z
+
+    z = precond(r)
+    rho = dsys.dot(r, z)
+    st["preconditioned_history"].append(rho)
+    d = z.clone()
+    for _ in range(max_iter):
+        q = dsys.apply(d)
+        st["mv_count"] += 1
+        dq = dsys.dot(d, q)
+        if not np.isfinite(dq) or dq <= 0.0:
+            raise RuntimeError(f"conjugate gradient breakdown: curvature {dq}")
+        alpha = rho / dq
+        x = x + alpha * d
+        r = r - alpha * q
+        st["iterations"] += 1
+        rel = dsys.dot(r, r) ** 0.5 / nb
+        st["residual_history"].append(rel)
+        if rel <= tol:
+            st["converged"] = True
+            break
+        z = precond(r)
+        rho_next = dsys.dot(r, z)
+        st["preconditioned_history"].append(rho_next)
+        beta = rho_next / rho
+        rho = rho_next
+        d = z + beta * d
+    if not st["converged"]:
+        raise RuntimeError(f"PCG did not reach tol={tol} within {max_iter} iterations")
+    return dsys.normalize(x), st
+
+
+class NativeBackend:
+    """Local compute in the sm_100a library (SpMV, inner solves)."""
+
+    def __init__(self):
+        from . import _lib
+        from .system import NativeCsr
+
+        self._lib = _lib
+        self._csr = NativeCsr
+        self.ctx = _lib.Context.default()
+
+    def matrix(self, a):
+        return self._csr(self.ctx, sp.csr_matrix(a))
+
+    def spmv(self, h, x):
+        return h.matvec(x.contiguous())
+
+    def inner(self, kind, a):
+        from .precond import make_inner
+
+        p = make_inner(kind)
+        p.setup(a)
+        return p
+
+    def inner_apply(self, h, y):
+        return h.apply_inverse(y.contiguous())
