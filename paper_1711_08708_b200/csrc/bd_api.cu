@@ -470,6 +470,9 @@ bd_status launch_tiled(bd_inner* p, const DevTile& t, const Rhs& rhs, double* xg
   return BD_OK;
 }
 
+bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, const Ctl& c,
+                     int ctr, int fin, int slot, int slot2, int64_t nmean);
+
 // ---- inner solve dispatch -----------------------------------------------------
 // Solve P x = rhs for one inner preconditioner inside control block c.
 // x_int: polled internal output (sentinel-filled here); out (nullable):
@@ -497,9 +500,12 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
     LAUNCHED(ctx);
     dev::k_trsv_persist<G, dev::RhsGather><<<p->EU.grid, dev::TPB, 0, st>>>(
-        p->EU.dev(), dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, p->EU.nchunks, fin, slot,
+        p->EU.dev(), dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, p->EU.nchunks, -1, slot,
         slot2, nmean);
     LAUNCHED(ctx);
+    // the mean of the output as a separate fixed-order pass: a per-chunk block
+    // reduction inside the solve would sit on its critical path
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->tiled) {
