@@ -1076,6 +1076,30 @@ struct EllTri {
   int ntasks;
 };
 
+// Staggered polling: keep several polls of the same word in flight, issued
+// ~STAGGER ns apart, so a value that lands is seen about one one-way L2
+// latency later instead of up to a full round trip.
+__device__ __forceinline__ long long ld_relaxed_bits(const double* p) {
+  long long b;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  return b;
+}
+__device__ __forceinline__ double spin_load_staggered(const double* p) {
+  long long b0 = ld_relaxed_bits(p);
+  if (b0 != SENTINEL) return __longlong_as_double(b0);
+  for (;;) {
+    __nanosleep(60);
+    const long long b1 = ld_relaxed_bits(p);
+    __nanosleep(60);
+    const long long b2 = ld_relaxed_bits(p);
+    __nanosleep(60);
+    const long long b3 = ld_relaxed_bits(p);
+    if (b1 != SENTINEL) return __longlong_as_double(b1);
+    if (b2 != SENTINEL) return __longlong_as_double(b2);
+    if (b3 != SENTINEL) return __longlong_as_double(b3);
+  }
+}
+
 __device__ __forceinline__ double spin_load_backoff(const double* p) {
   long long b;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
@@ -1124,7 +1148,11 @@ __global__ void __launch_bounds__(TPB) k_trsv_persist(EllTri t, Rhs rhs, double*
     Pre nx;
     load(next, nx);
     double a = 0.0;
+#ifdef BD_STAGGER
+    if (cur.col >= 0) a = cur.val * spin_load_staggered(&y[cur.col]);
+#else
     if (cur.col >= 0) a = cur.val * spin_load(&y[cur.col]);
+#endif
     a = group_sum<G>(a);  // every lane of the warp reaches the shuffle
     double val = 0.0;
     if (cur.row >= 0) {

@@ -48,7 +48,7 @@ def main():
            "checksum_S1": float(np.abs(sysm.stiff_total.data).sum()),
            "checksum_Km": float(np.abs(km.data).sum()), "probes": wl.probes.tolist(),
            "tol": wl.tol, "dt": wl.dt, "iters": [], "step_s": [], "trace": [], "u_norm": [],
-           "v_norm": []}
+           "v_norm": [], "sub_stride": 97, "u_sub": [], "v_sub": []}
     print(json.dumps({k: v for k, v in rec.items() if not isinstance(v, list)}), flush=True)
     n, m = sysm.n, sysm.n_heart
     state = (np.zeros(n), np.full(m, wl.ionic.v_rest), np.ones(m))
@@ -67,6 +67,9 @@ def main():
         rec["trace"].append(state[1][wl.probes].tolist())
         rec["u_norm"].append(float(np.linalg.norm(state[0])))
         rec["v_norm"].append(float(np.linalg.norm(state[1])))
+        if k < 3:  # strided subsample of the state for a rel-L2 check
+            rec["u_sub"].append(state[0][::97].tolist())
+            rec["v_sub"].append(state[1][::97].tolist())
         print(f"step {k + 1}: {st['iterations']} it, {rec['step_s'][-1]:.1f}s", flush=True)
         with open(out_path, "w") as fh:
             json.dump(rec, fh)
