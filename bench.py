@@ -285,8 +285,8 @@ def run_native(args, rank, world, local_rank):
                     "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_in,
                     "wall_s": round(wall_e2e, 3)},
             "roofline": {"bound": "hbm",
-                         "kernel": "bulk IC(0) triangular solve pair (k_trsv_fwd + k_trsv_bwd, "
-                                   "P_1 block)" if wl.inner != "jacobi" else "jacobi",
+                         "kernel": ("bulk inner solve pair: forward + backward triangular pass "
+                                    "(k_trsv_persist, P_1 block)") if wl.inner != "jacobi" else "jacobi",
                          "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
