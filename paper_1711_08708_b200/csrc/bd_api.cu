@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -95,12 +96,22 @@ struct DevEll {
   dev::EllTri dev() const { return dev::EllTri{task_row, task_diag, ell_col, ell_val, ntasks}; }
 };
 
+struct DevSuper {
+  int* sn_start = nullptr;
+  int* sn_size = nullptr;
+  int* task_sn = nullptr;
+  int ntasks = 0;
+  int grid = 0;
+};
+
 struct bd_inner {
   bd_ctx* ctx;
   int kind;
   int64_t n;
   int G = 8;
   DevTri L, U;
+  bool super = false;
+  DevSuper SL, SU;
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
   bool persist = false;
@@ -432,6 +443,117 @@ void free_ell(DevEll* e) {
   cudaFree(e->ell_val);
 }
 
+// Supernodes of a lower CSR factor (diagonal last): maximal runs of rows whose
+// mutual dependencies form a dense triangle; then level-ordered task lists
+// for the forward (L) and backward (U = L^T) passes.
+bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw) {
+  const int64_t n = L.n;
+  std::vector<int32_t> start, size, sn_of(n);
+  int32_t c0 = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    bool join = false;
+    const int64_t k = i - c0;
+    if (i > 0 && k < dev::SN_MAX) {
+      const int64_t e = L.indptr[i + 1], off = e - 1 - L.indptr[i];
+      if (off >= k && k > 0)
+        join = L.indices[e - 1 - k] == c0 && L.indices[e - 2] == (int32_t)(i - 1);
+    }
+    if (!join) {
+      if (i > 0) size.push_back((int32_t)(i - c0));
+      c0 = (int32_t)i;
+      start.push_back(c0);
+    }
+    sn_of[i] = (int32_t)start.size() - 1;
+  }
+  size.push_back((int32_t)(n - c0));
+  const int64_t ns = (int64_t)start.size();
+  // forward levels: external columns (< start) point to earlier supernodes
+  std::vector<int32_t> lvf(ns, 0), lvb(ns, 0);
+  for (int64_t s = 0; s < ns; ++s) {
+    int32_t lv = 0;
+    for (int64_t i = start[s]; i < start[s] + size[s]; ++i)
+      for (int64_t q = L.indptr[i]; q < L.indptr[i + 1]; ++q) {
+        const int32_t j = L.indices[q];
+        if (j < start[s]) lv = std::max(lv, lvf[sn_of[j]] + 1);
+      }
+    lvf[s] = lv;
+  }
+  // backward levels: supernode s depends on the supernodes of rows j > end that
+  // have s-rows in their pattern (U = L^T): propagate from L's rows
+  {
+    // dependency t -> s for every external entry (i in t, j in s, j < start[t])
+    std::vector<std::vector<int32_t>> users(ns);
+    for (int64_t t = 0; t < ns; ++t)
+      for (int64_t i = start[t]; i < start[t] + size[t]; ++i)
+        for (int64_t q = L.indptr[i]; q < L.indptr[i + 1]; ++q) {
+          const int32_t j = L.indices[q];
+          if (j < start[t]) {
+            auto& u = users[sn_of[j]];
+            if (u.empty() || u.back() != (int32_t)t) u.push_back((int32_t)t);
+          }
+        }
+    for (int64_t s = ns - 1; s >= 0; --s) {
+      int32_t lv = 0;
+      for (int32_t t : users[s]) lv = std::max(lv, lvb[t] + 1);
+      lvb[s] = lv;
+    }
+  }
+  auto order = [&](const std::vector<int32_t>& lv, DevSuper* out) -> bd_status {
+    std::vector<int32_t> idx(ns);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return lv[a] < lv[b]; });
+    std::vector<int32_t> st(ns), sz(ns), tasks;
+    for (int64_t k = 0; k < ns; ++k) {
+      st[k] = start[idx[k]];
+      sz[k] = size[idx[k]];
+    }
+    // tasks: a big supernode alone, or up to 16 small ones of the same level
+    for (int64_t k = 0; k < ns;) {
+      tasks.push_back((int32_t)k);
+      if (sz[k] > 32) {
+        ++k;
+        continue;
+      }
+      int64_t e = k + 1;
+      while (e < ns && e - k < 16 && sz[e] <= 32 && lv[idx[e]] == lv[idx[k]]) ++e;
+      k = e;
+    }
+    tasks.push_back((int32_t)ns);
+    CK(ctx, upload_vec(&out->sn_start, st));
+    CK(ctx, upload_vec(&out->sn_size, sz));
+    CK(ctx, upload_vec(&out->task_sn, tasks));
+    out->ntasks = (int)tasks.size() - 1;
+    out->grid = (int)std::max<int64_t>(1, std::min<int64_t>(out->ntasks, (int64_t)ctx->nsm * 2));
+    return BD_OK;
+  };
+  TRY(order(lvf, fw));
+  TRY(order(lvb, bw));
+  if (getenv("BD_DEBUG")) {
+    int64_t big = 0, maxsz = 0, rows_big = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+      maxsz = std::max<int64_t>(maxsz, size[s]);
+      if (size[s] >= 32) {
+        ++big;
+        rows_big += size[s];
+      }
+    }
+    const int32_t df = *std::max_element(lvf.begin(), lvf.end()) + 1;
+    const int32_t db = *std::max_element(lvb.begin(), lvb.end()) + 1;
+    std::fprintf(stderr,
+                 "[bd] supernodes n=%lld count=%lld (>=32 rows: %lld covering %lld rows) max=%lld "
+                 "levels fwd=%d bwd=%d\n",
+                 (long long)n, (long long)ns, (long long)big, (long long)rows_big,
+                 (long long)maxsz, df, db);
+  }
+  return BD_OK;
+}
+
+void free_super(DevSuper* s) {
+  cudaFree(s->sn_start);
+  cudaFree(s->sn_size);
+  cudaFree(s->task_sn);
+}
+
 template <int G, class Rhs>
 bd_status launch_tiled(bd_inner* p, const DevTile& t, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr, int fin, int slot, int slot2, int64_t nmean) {
@@ -488,6 +610,25 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->super) {
+    // exact factor: supernodal forward / backward passes
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::SuperTri tl{(int)p->n,        p->L.rowptr,  p->L.col,    p->L.val, p->SL.sn_start,
+                     p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr};
+    dev::k_trsv_super<true, Rhs><<<p->SL.grid, 512, 0, st>>>(tl, rhs, p->y_int, nullptr, c, ctr0,
+                                                              ctr0 + 1);
+    LAUNCHED(ctx);
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(x_int, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
+                     p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm};
+    dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
+        tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
+    LAUNCHED(ctx);
+    if (fin >= 0) TRY(launch_dot(ctx, x_int, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->persist) {
@@ -1037,6 +1178,13 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   p->G = pick_g(avg - 1.0);
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
+  if (st == BD_OK && kind == BD_INNER_EXACT) {
+    const char* m = getenv("BD_EXACT_TRSV");
+    if (!(m && std::string(m) == "rows")) {
+      st = build_super(ctx, lower, &p->SL, &p->SU);
+      if (st == BD_OK) p->super = true;
+    }
+  }
   if (st == BD_OK && kind == BD_INNER_IC0) {
     const char* mode = getenv("BD_TRSV");
     const std::string m = mode ? mode : "persist";
@@ -1088,6 +1236,8 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_tile(&p->TU);
   free_ell(&p->EL);
   free_ell(&p->EU);
+  free_super(&p->SL);
+  free_super(&p->SU);
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);

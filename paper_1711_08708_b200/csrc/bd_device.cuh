@@ -1189,6 +1189,274 @@ __global__ void __launch_bounds__(TPB) k_trsv_persist(EllTri t, Rhs rhs, double*
   }
 }
 
+// ---- supernodal triangular solve (exact / Cholesky factors) -----------------------
+// A supernode is a run of consecutive rows [c0, c0+ns) whose mutual
+// dependencies form a dense triangle (the separators of a nested-dissection
+// factor).  One CTA owns a supernode task: (1) the external sparse dots of all
+// its rows in parallel (warp per row, polling only other supernodes), then
+// (2) the dense diagonal block in 32-row panels: one warp solves a panel with
+// shuffles, all warps update the remaining rows.  Tasks (supernodes in DAG
+// level order) are taken in order by a persistent grid, so the row-level
+// chain through a separator no longer costs one cross-SM round trip per row.
+struct SuperTri {
+  int n;
+  const int* rowptr;
+  const int* col;
+  const double* val;
+  const int* sn_start;  // per supernode (level order): first row
+  const int* sn_size;   // per supernode: rows
+  const int* task_sn;   // per task: first supernode; tasks = [task_sn[t], task_sn[t+1])
+  int ntasks;           // a task is either ONE big supernode (> 32 rows) or up to
+                        // 16 small independent ones (same level), one per warp
+  const int* perm;      // nullable: scatter of the output (original order)
+};
+
+constexpr int SN_MAX = 1024;
+
+// One warp solves one small supernode (<= 32 rows): external dots RW rows at
+// a time, then the dense triangle with the coefficients in registers.
+template <bool LOWER, class Rhs>
+__device__ __forceinline__ void super_small_warp(const SuperTri& t, const Rhs& rhs,
+                                                 double* __restrict__ x,
+                                                 double* __restrict__ out, int c0, int ns,
+                                                 int lane) {
+  const int c1 = c0 + ns;
+  // lane l owns the l-th row in solve order: its right-hand side minus its
+  // external part, entries walked sequentially, 4 loads in flight
+  double ri = 0.0;
+  {
+    const int k = LOWER ? lane : ns - 1 - lane;
+    const bool ok = lane < ns;
+    const int i = ok ? c0 + k : -1;
+    int eb = 0, ee = 0;
+    if (ok) {
+      const int b = t.rowptr[i], e = t.rowptr[i + 1];
+      eb = LOWER ? b : b + (c1 - i);
+      ee = LOWER ? e - 1 - k : e;
+    }
+    double acc = 0.0;
+    for (int q = eb; q < ee; q += 4) {
+      int cl[4];
+      double vl[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool in = q + u < ee;
+        cl[u] = in ? t.col[q + u] : -1;
+        vl[u] = in ? t.val[q + u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = ld_relaxed_if(&x[cl[u] < 0 ? 0 : cl[u]], cl[u] >= 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double d = xv[u];
+        if (cl[u] >= 0 && __double_as_longlong(d) == SENTINEL) d = spin_load(&x[cl[u]]);
+        acc = fma(vl[u], d, acc);
+      }
+    }
+    const double bi = rhs.template eval<1>(i, 0);
+    if (ok) ri = __dsub_rn(bi, acc);
+  }
+  // dense triangle: lane l owns the l-th row in solve order
+  const bool ok = lane < ns;
+  const int k = LOWER ? lane : ns - 1 - lane;
+  const int i = ok ? c0 + k : c0;
+  double diag = 1.0;
+  double a[32];
+  int base = 0;
+  if (ok) {
+    const int b = t.rowptr[i], e = t.rowptr[i + 1];
+    diag = LOWER ? t.val[e - 1] : t.val[b];
+    base = LOWER ? (e - 1 - k) : b;
+  }
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    a[jj] = 0.0;
+    if (ok && jj < lane) {
+      const int kj = LOWER ? jj : ns - 1 - jj;
+      const int j = c0 + kj;
+      a[jj] = LOWER ? t.val[base + (j - c0)] : t.val[base + (j - i)];
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    if (jj >= ns) break;
+    const double rj = __shfl_sync(0xffffffffu, ri, jj);
+    const double dj = __shfl_sync(0xffffffffu, diag, jj);
+    const double xj = __ddiv_rn(rj, dj);
+    if (lane == jj) ri = xj;
+    if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(a[jj], xj));
+  }
+  if (ok) {
+    publish(&x[i], ri);
+    if (out) out[t.perm ? t.perm[i] : i] = ri;
+  }
+}
+
+template <bool LOWER, class Rhs>
+__global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double* __restrict__ x,
+                                                    double* __restrict__ out, Ctl c, int ctr_task,
+                                                    int ctr_done) {
+  if (inactive(c)) return;
+  constexpr int RW = 4;  // rows per warp in flight
+  __shared__ double r[SN_MAX];
+  __shared__ double panel[32][33];
+  __shared__ int task_s;
+  __shared__ int last_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+    __syncthreads();
+    const int task = task_s;
+    __syncthreads();
+    if (task >= t.ntasks) break;
+    const int s0 = t.task_sn[task], s1 = t.task_sn[task + 1];
+    unsigned long long t_beg = 0;
+    unsigned long long* trace = g_tile_trace;
+    if (trace && threadIdx.x == 0) t_beg = gtimer();
+    if (s1 - s0 > 1 || t.sn_size[s0] <= 32) {
+      // group of small independent supernodes: one warp each, no CTA barrier
+      if (s0 + warp < s1)
+        super_small_warp<LOWER>(t, rhs, x, out, t.sn_start[s0 + warp], t.sn_size[s0 + warp], lane);
+      if (trace) {
+        __syncthreads();
+        if (threadIdx.x == 0 && task < g_tile_trace_steps) {
+          trace[task * 4 + 0] = t_beg;
+          trace[task * 4 + 1] = gtimer();
+          trace[task * 4 + 2] = blockIdx.x;
+          trace[task * 4 + 3] = (unsigned long long)(s1 - s0);
+        }
+      }
+      continue;
+    }
+    const int c0 = t.sn_start[s0], ns = t.sn_size[s0], c1 = c0 + ns;
+    // (1) right-hand side minus the external part, RW rows per warp in flight
+    for (int k0 = warp * RW; k0 < ns; k0 += nw * RW) {
+      int eb[RW], ee[RW];
+      double sacc[RW];
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        const int k = k0 + u;
+        sacc[u] = 0.0;
+        eb[u] = ee[u] = 0;
+        if (k < ns) {
+          const int i = c0 + k;
+          const int b = t.rowptr[i], e = t.rowptr[i + 1];
+          eb[u] = LOWER ? b : b + (c1 - i);
+          ee[u] = LOWER ? e - 1 - k : e;
+        }
+      }
+      int len = 0;
+#pragma unroll
+      for (int u = 0; u < RW; ++u) len = max(len, ee[u] - eb[u]);
+      for (int q = lane; q < len; q += 32) {
+        int cl[RW];
+        double vl[RW], xv[RW];
+#pragma unroll
+        for (int u = 0; u < RW; ++u) {
+          const bool ok = eb[u] + q < ee[u];
+          cl[u] = ok ? t.col[eb[u] + q] : -1;
+          vl[u] = ok ? t.val[eb[u] + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RW; ++u) xv[u] = ld_relaxed_if(&x[cl[u] < 0 ? 0 : cl[u]], cl[u] >= 0);
+#pragma unroll
+        for (int u = 0; u < RW; ++u) {
+          double d = xv[u];
+          if (cl[u] >= 0 && __double_as_longlong(d) == SENTINEL) d = spin_load(&x[cl[u]]);
+          sacc[u] = fma(vl[u], d, sacc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        const double sum = group_sum<32>(sacc[u]);
+        const int k = k0 + u;
+        const double bi = rhs.template eval<32>(k < ns ? c0 + k : -1, lane);
+        if (lane == 0 && k < ns) r[k] = __dsub_rn(bi, sum);
+      }
+    }
+    __syncthreads();
+    unsigned long long t_ext = 0;
+    if (trace && threadIdx.x == 0) t_ext = gtimer();
+    // (2) dense block, left-looking 32-row panels (solve order: ascending rows
+    //     for L, descending for U).  r[k] holds row k's rhs, then its solution.
+    for (int p0 = 0; p0 < ns; p0 += 32) {
+      const int pn = min(32, ns - p0);
+      // (a) panel rows minus the already solved rows [0, p0) of the block
+      if (p0 > 0) {
+        for (int w = warp; w < pn; w += nw) {
+          const int k = LOWER ? p0 + w : ns - 1 - (p0 + w);
+          const int i = c0 + k;
+          const int b = t.rowptr[i], e = t.rowptr[i + 1];
+          double s = 0.0;
+          for (int jj = lane; jj < p0; jj += 32) {
+            const int kj = LOWER ? jj : ns - 1 - jj;
+            const int j = c0 + kj;
+            const int pos = LOWER ? (e - 1 - k) + (j - c0) : b + (j - i);
+            s = fma(t.val[pos], r[kj], s);
+          }
+          s = group_sum<32>(s);
+          if (lane == 0) r[k] = __dsub_rn(r[k], s);
+        }
+        __syncthreads();
+      }
+      // (b) the panel triangle, one warp, coefficients in shared memory
+      if (warp == 0) {
+        const int k = LOWER ? p0 + lane : ns - 1 - (p0 + lane);
+        const bool ok = lane < pn;
+        const int i = ok ? c0 + k : c0;
+        double diag = 1.0;
+        if (ok) {
+          const int b = t.rowptr[i], e = t.rowptr[i + 1];
+          diag = LOWER ? t.val[e - 1] : t.val[b];
+          const int base = LOWER ? (e - 1 - k) : b;
+#pragma unroll 8
+          for (int jj = 0; jj < 32; ++jj) {
+            double a = 0.0;
+            if (jj < lane) {
+              const int kj = LOWER ? p0 + jj : ns - 1 - (p0 + jj);
+              const int j = c0 + kj;
+              a = LOWER ? t.val[base + (j - c0)] : t.val[base + (j - i)];
+            }
+            panel[lane][jj] = a;
+          }
+        }
+        double ri = ok ? r[k] : 0.0;
+        __syncwarp();
+        for (int jj = 0; jj < pn; ++jj) {
+          const double rj = __shfl_sync(0xffffffffu, ri, jj);
+          const double dj = __shfl_sync(0xffffffffu, diag, jj);
+          const double xj = __ddiv_rn(rj, dj);
+          if (lane == jj) ri = xj;
+          if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(panel[lane][jj], xj));
+        }
+        if (ok) {
+          r[k] = ri;
+          publish(&x[i], ri);
+          if (out) out[t.perm ? t.perm[i] : i] = ri;
+        }
+      }
+      __syncthreads();
+    }
+    if (trace && threadIdx.x == 0 && task < g_tile_trace_steps) {
+      trace[task * 4 + 0] = t_beg;
+      trace[task * 4 + 1] = gtimer();
+      trace[task * 4 + 2] = blockIdx.x;
+      trace[task * 4 + 3] = ((t_ext - t_beg) << 20) | (1u << 19) | (unsigned)ns;
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && threadIdx.x == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
+}
+
 // Jacobi "solve": out_i = inv_i * rhs_i (bd/precond.py:231-232), with the
 // same rhs functors and the optional mean reduction.
 template <int G, class Rhs>
