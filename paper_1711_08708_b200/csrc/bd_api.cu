@@ -96,6 +96,29 @@ struct DevEll {
   dev::EllTri dev() const { return dev::EllTri{task_row, task_diag, ell_col, ell_val, ntasks}; }
 };
 
+constexpr int kClusterParts = 16;
+constexpr int kClusterStages = 3;
+constexpr int kClusterStagesDeep = 10;
+
+struct DevCluster {
+  int* lvl_ptr = nullptr;
+  int* task_row = nullptr;
+  double* task_diag = nullptr;
+  double* ell_val = nullptr;
+  short* ell_code = nullptr;
+  int* exp_ptr = nullptr;
+  int* exp_src = nullptr;
+  int* exp_dst = nullptr;
+  int nlevels = 0, W = 4, wmax = 0, rmax = 0, emax = 0, E = 8;
+  size_t smem = 0;
+  bool deep = false;
+  int64_t ntasks = 0;
+  dev::ClusterDev dev() const {
+    return dev::ClusterDev{lvl_ptr, task_row, task_diag, ell_val, ell_code, exp_ptr,
+                           exp_src, exp_dst, nlevels, W, wmax, rmax, emax};
+  }
+};
+
 struct DevSuper {
   int* sn_start = nullptr;
   int* sn_size = nullptr;
@@ -112,6 +135,9 @@ struct bd_inner {
   DevTri L, U;
   bool super = false;
   DevSuper SL, SU;
+  bool cluster = false;
+  DevCluster CL, CU;
+  double* rtmp = nullptr;
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
   bool persist = false;
@@ -554,6 +580,113 @@ void free_super(DevSuper* s) {
   cudaFree(s->task_sn);
 }
 
+bd_status upload_cluster(bd_ctx* ctx, const ClusterSchedule& cs, DevCluster* out) {
+  CK(ctx, upload_vec(&out->lvl_ptr, cs.lvl_ptr));
+  CK(ctx, upload_vec(&out->task_row, cs.task_row));
+  CK(ctx, upload_vec(&out->task_diag, cs.task_diag));
+  CK(ctx, upload_vec(&out->ell_val, cs.ell_val));
+  std::vector<short> code(cs.ell_code.begin(), cs.ell_code.end());
+  CK(ctx, upload_vec(&out->ell_code, code));
+  CK(ctx, upload_vec(&out->exp_ptr, cs.exp_ptr));
+  CK(ctx, upload_vec(&out->exp_src, cs.exp_src));
+  CK(ctx, upload_vec(&out->exp_dst, cs.exp_dst));
+  out->nlevels = cs.nlevels;
+  out->W = cs.W;
+  out->wmax = cs.wmax;
+  out->rmax = cs.rmax;
+  out->emax = std::max(cs.emax, 4);
+  out->E = cs.E;
+  out->ntasks = (int64_t)cs.task_row.size();
+  out->smem = dev::cl_smem_bytes(out->rmax, out->emax, out->wmax, out->W, out->E,
+                                 kClusterStagesDeep, out->nlevels);
+  out->deep = true;
+  if (out->smem + 1024 > 232448) {
+    out->deep = false;
+    out->smem = dev::cl_smem_bytes(out->rmax, out->emax, out->wmax, out->W, out->E, kClusterStages,
+                                   out->nlevels);
+  }
+  return BD_OK;
+}
+
+void free_cluster(DevCluster* c) {
+  cudaFree(c->lvl_ptr);
+  cudaFree(c->task_row);
+  cudaFree(c->task_diag);
+  cudaFree(c->ell_val);
+  cudaFree(c->ell_code);
+  cudaFree(c->exp_ptr);
+  cudaFree(c->exp_src);
+  cudaFree(c->exp_dst);
+}
+
+// Cluster-wavefront schedules for an IC(0)-like factor; leaves p->cluster false
+// (with the reason under BD_DEBUG) when the structure does not qualify.
+bd_status setup_cluster(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
+                        const double* coords, int dim) {
+  bd_ctx* ctx = p->ctx;
+  const int P = kClusterParts;
+  if (lower.n < 64 * P) return BD_OK;
+  std::vector<int32_t> part;
+  if (coords && dim > 0)
+    partition_coords(lower.n, dim, coords, P, &part);
+  else
+    partition_rows(lower, P, &part);
+  int E = 4;
+  for (int64_t i = 0; i < lower.n; ++i)
+    while (E < lower.indptr[i + 1] - lower.indptr[i] - 1) E <<= 1;
+  for (int64_t i = 0; i < upper.n; ++i)
+    while (E < upper.indptr[i + 1] - upper.indptr[i] - 1) E <<= 1;
+  if (E > 8) return BD_OK;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  ClusterSchedule cl, cu;
+  std::string why;
+  bool ok = build_cluster_schedule(lower, true, part, P, E, 4, 4096, 8192, &cl, &why) &&
+            build_cluster_schedule(upper, false, part, P, E, 4, 4096, 8192, &cu, &why);
+  if (ok) {
+    TRY(upload_cluster(ctx, cl, &p->CL));
+    TRY(upload_cluster(ctx, cu, &p->CU));
+    if (std::max(p->CL.smem, p->CU.smem) + 1024 > (size_t)max_smem) {
+      ok = false;
+      why = "shared memory";
+    }
+  }
+  if (getenv("BD_DEBUG"))
+    std::fprintf(stderr, "[bd] cluster schedule n=%lld: %s (levels %d, rmax %d, wmax %d, smem %zu)\n",
+                 (long long)lower.n, ok ? "ok" : why.c_str(), cl.nlevels, cl.rmax, cl.wmax,
+                 std::max(p->CL.smem, p->CU.smem));
+  if (!ok) return BD_OK;
+  CK(ctx, dalloc(&p->rtmp, std::max(p->CL.ntasks, p->CU.ntasks)));
+  p->cluster = true;
+  p->G = E;
+  return BD_OK;
+}
+
+template <int E, class Rhs>
+bd_status launch_cluster(bd_inner* p, const DevCluster& cd, const Rhs& rhs, double* xg,
+                         const Ctl& c) {
+  bd_ctx* ctx = p->ctx;
+  auto kern = cd.deep ? dev::k_trsv_cluster<E, kClusterStagesDeep, Rhs>
+                     : dev::k_trsv_cluster<E, kClusterStages, Rhs>;
+  CK(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cd.smem));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kClusterParts;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterParts);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = cd.smem;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(ctx, cudaLaunchKernelEx(&cfg, kern, cd.dev(), rhs, xg, p->rtmp, c));
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
 template <int G, class Rhs>
 bd_status launch_tiled(bd_inner* p, const DevTile& t, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr, int fin, int slot, int slot2, int64_t nmean) {
@@ -610,6 +743,18 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->cluster) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    if (p->G == 4) {
+      TRY(launch_cluster<4>(p, p->CL, rhs, p->y_int, c));
+      TRY(launch_cluster<4>(p, p->CU, dev::RhsGather{p->y_int}, xg, c));
+    } else {
+      TRY(launch_cluster<8>(p, p->CL, rhs, p->y_int, c));
+      TRY(launch_cluster<8>(p, p->CU, dev::RhsGather{p->y_int}, xg, c));
+    }
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->super) {
@@ -1188,10 +1333,13 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   if (st == BD_OK && kind == BD_INNER_IC0) {
     const char* mode = getenv("BD_TRSV");
     const std::string m = mode ? mode : "persist";
+    if (m == "cluster") {
+      st = setup_cluster(p, lower, upper, coords, dim);
+    }
     if (m == "tiled" || m == "rows") {
       p->rows_mode = (m == "rows");
       st = setup_tiles(p, lower, upper, coords, dim);
-    } else if (m == "persist") {
+    } else if (m == "persist" || (m == "cluster" && !p->cluster)) {
       int64_t maxoff = 0;
       for (int64_t i = 0; i < n; ++i)
         maxoff = std::max<int64_t>(maxoff, lower.indptr[i + 1] - lower.indptr[i] - 1);
@@ -1238,6 +1386,9 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_ell(&p->EU);
   free_super(&p->SL);
   free_super(&p->SU);
+  free_cluster(&p->CL);
+  free_cluster(&p->CU);
+  cudaFree(p->rtmp);
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);

@@ -1061,6 +1061,168 @@ __global__ void __launch_bounds__(512, 1) k_trsv_rows(TileDev T, Rhs rhs, double
   }
 }
 
+// ---- cluster-wavefront triangular solve ----------------------------------------
+// One thread-block cluster (P CTAs, one part each) steps through the global
+// levels in lockstep: per level, every CTA solves its own rows (thread per
+// row) reading dependencies from a ring of W level windows in shared memory,
+// pushes the values its neighbours import into THEIR windows through
+// distributed shared memory, and the cluster barrier publishes everything.
+// The per-level ELL block (values, int16 window codes, diagonal, right-hand
+// side, row ids, export list) streams through a D-stage cp.async ring.
+struct ClusterDev {
+  const int* lvl_ptr;     // parts*(nlevels+1)
+  const int* task_row;
+  const double* task_diag;
+  const double* ell_val;  // ntasks*E
+  const short* ell_code;  // ntasks*E
+  const int* exp_ptr;     // parts*(nlevels+1)
+  const int* exp_src;
+  const int* exp_dst;
+  int nlevels, W, wmax, rmax, emax;
+};
+
+__host__ __device__ constexpr size_t cl_stage_bytes(int rmax, int emax, int E) {
+  return (size_t)rmax * (E * 10 + 20) + (size_t)emax * 8;
+}
+__host__ __device__ constexpr size_t cl_ring_offset(int wmax, int W) {
+  return ((size_t)W * wmax * 8 + 15) & ~(size_t)15;
+}
+__host__ __device__ constexpr size_t cl_smem_bytes(int rmax, int emax, int wmax, int W, int E,
+                                                   int D, int nlevels) {
+  return cl_ring_offset(wmax, W) + (size_t)D * cl_stage_bytes(rmax, emax, E) +
+         (size_t)(nlevels + 1) * 8 + 16;
+}
+
+template <int E, int D, class Rhs>
+__global__ void __launch_bounds__(1024, 1) k_trsv_cluster(ClusterDev S, Rhs rhs, double* __restrict__ xg,
+                                                          double* __restrict__ rtmp, Ctl c) {
+  namespace cg = cooperative_groups;
+  if (inactive(c)) return;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int p = (int)cluster.block_rank();
+  const int NL = S.nlevels;
+  double* win = reinterpret_cast<double*>(smem_raw);
+  unsigned char* ring = smem_raw + cl_ring_offset(S.wmax, S.W);
+  const size_t sb = cl_stage_bytes(S.rmax, S.emax, E);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  // per-level row / export offsets of this part, in shared memory
+  int* lp = reinterpret_cast<int*>(ring + (size_t)D * sb);
+  int* ep = lp + (NL + 1);
+  for (int k = tid; k <= NL; k += nth) {
+    lp[k] = S.lvl_ptr[(size_t)p * (NL + 1) + k];
+    ep[k] = S.exp_ptr[(size_t)p * (NL + 1) + k];
+  }
+  __syncthreads();
+  // prologue: right-hand side of every own row (task order), zero windows
+  {
+    const int t0 = lp[0], t1 = lp[NL];
+    constexpr int U = 4;
+    for (int base = t0; base < t1; base += U * nth) {
+      int row[U];
+      double b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + u * nth + tid;
+        row[u] = k < t1 ? S.task_row[k] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = rhs.template eval<1>(row[u], 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + u * nth + tid;
+        if (k < t1) rtmp[k] = b[u];
+      }
+    }
+    for (int k = tid; k < S.W * S.wmax; k += nth) win[k] = 0.0;
+  }
+  __threadfence();
+  __syncthreads();
+  auto issue = [&](int L) {
+    if (L < NL) {
+      unsigned char* st = ring + (size_t)(L % D) * sb;
+      const int a = lp[L], n = lp[L + 1] - a;  // n is a multiple of 8
+      const int ea = ep[L], ne = ep[L + 1] - ea;  // multiple of 4
+      double* sv = reinterpret_cast<double*>(st);
+      short* sc = reinterpret_cast<short*>(st + (size_t)S.rmax * E * 8);
+      double* sd = reinterpret_cast<double*>(st + (size_t)S.rmax * E * 10);
+      double* sr = sd + S.rmax;
+      int* srow = reinterpret_cast<int*>(sr + S.rmax);
+      int* ssrc = srow + S.rmax;
+      int* sdst = ssrc + S.emax;
+      for (int q = tid; q < n * E / 2; q += nth) cp_async16(sv + 2 * q, S.ell_val + (size_t)a * E + 2 * q);
+      for (int q = tid; q < n * E / 8; q += nth) cp_async16(sc + 8 * q, S.ell_code + (size_t)a * E + 8 * q);
+      for (int q = tid; q < n / 2; q += nth) {
+        cp_async16(sd + 2 * q, S.task_diag + a + 2 * q);
+        cp_async16(sr + 2 * q, rtmp + a + 2 * q);
+      }
+      for (int q = tid; q < n / 4; q += nth) cp_async16(srow + 4 * q, S.task_row + a + 4 * q);
+      for (int q = tid; q < ne / 4; q += nth) {
+        cp_async16(ssrc + 4 * q, S.exp_src + ea + 4 * q);
+        cp_async16(sdst + 4 * q, S.exp_dst + ea + 4 * q);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int L = 0; L < D - 1; ++L) issue(L);
+  cp_async_wait<D - 2>();  // own copies of level 0 landed
+  cluster.sync();           // every CTA resident and initialised; level-0 data visible
+  unsigned long long* trace = g_tile_trace;
+  const bool tr_on = trace && p == 0 && tid == 0;
+  for (int L = 0; L < NL; ++L) {
+    long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+    if (tr_on) c0 = clock64();
+    issue(L + D - 1);
+    if (tr_on) c1 = clock64();
+    const unsigned char* st = ring + (size_t)(L % D) * sb;
+    const double* sv = reinterpret_cast<const double*>(st);
+    const short* sc = reinterpret_cast<const short*>(st + (size_t)S.rmax * E * 8);
+    const double* sd = reinterpret_cast<const double*>(st + (size_t)S.rmax * E * 10);
+    const double* sr = sd + S.rmax;
+    const int* srow = reinterpret_cast<const int*>(sr + S.rmax);
+    const int* ssrc = srow + S.rmax;
+    const int* sdst = ssrc + S.emax;
+    const int n = lp[L + 1] - lp[L];
+    double* wl = win + (size_t)(L % S.W) * S.wmax;
+    for (int r = tid; r < n; r += nth) {
+      const int row = srow[r];
+      if (row < 0) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int code = sc[r * E + e];
+        const double d = code >= 0 ? win[code] : 0.0;
+        acc = fma(sv[r * E + e], d, acc);
+      }
+      const double v = __ddiv_rn(__dsub_rn(sr[r], acc), sd[r]);
+      wl[r] = v;
+      xg[row] = v;
+    }
+    if (tr_on) c2 = clock64();
+    __syncthreads();
+    if (tr_on) c3 = clock64();
+    const int ne = ep[L + 1] - ep[L];
+    for (int e = tid; e < ne; e += nth) {
+      const int src = ssrc[e];
+      if (src < 0) continue;
+      const int dst = sdst[e];
+      double* remote = cluster.map_shared_rank(win, dst >> 16);
+      remote[dst & 0xffff] = wl[src];
+    }
+    if (tr_on) c4 = clock64();
+    cp_async_wait<D - 2>();  // own copies of level L+1 landed
+    if (tr_on) c5 = clock64();
+    cluster.sync();           // exports + next level's data visible
+    if (tr_on && L < g_tile_trace_steps) {
+      const long long c6 = clock64();
+      unsigned long long* q = trace + (size_t)L * 6;
+      q[0] = c1 - c0; q[1] = c2 - c1; q[2] = c3 - c2; q[3] = c4 - c3; q[4] = c5 - c4; q[5] = c6 - c5;
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ---- persistent sync-free triangular solve ----------------------------------
 // Tasks (rows) in level order, ELL entries (G per row, column -1 = padding)
 // stored in task order so a chunk of rows is one contiguous, coalesced read.

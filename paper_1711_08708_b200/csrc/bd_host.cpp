@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <numeric>
+#include <unordered_map>
 
 namespace bd {
 
@@ -661,6 +662,130 @@ bool build_tile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t
     }
     out->ell_col.swap(col2);
     out->ell_val.swap(val2);
+  }
+  return true;
+}
+
+}  // namespace bd
+
+// ---------------------------------------------------------------------------
+namespace bd {
+
+bool build_cluster_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& part,
+                            int parts, int E, int W, int cap_rows, int cap_slots,
+                            ClusterSchedule* out, std::string* why) {
+  const int64_t n = t.n;
+  std::vector<int32_t> level;
+  const int64_t nl = row_levels(t, lower, &level);
+  out->parts = parts;
+  out->E = E;
+  out->W = W;
+  out->nlevels = (int)nl;
+  // own rows per (part, level), in row order
+  std::vector<std::vector<int32_t>> own((size_t)parts * nl);
+  for (int64_t i = 0; i < n; ++i) own[(size_t)part[i] * nl + level[i]].push_back((int32_t)i);
+  // dependency distance check and import sets
+  std::vector<std::vector<int32_t>> imp((size_t)parts * nl);
+  for (int64_t i = 0; i < n; ++i) {
+    int cnt = 0;
+    for (int64_t q = t.indptr[i]; q < t.indptr[i + 1]; ++q) {
+      const int32_t j = t.indices[q];
+      if (j == i) continue;
+      if (++cnt > E) {
+        *why = "row longer than the ELL width";
+        return false;
+      }
+      const int d = level[i] - level[j];
+      if (d < 1 || d >= W) {
+        *why = "dependency outside the level window";
+        return false;
+      }
+      if (part[j] != part[i]) imp[(size_t)part[i] * nl + level[j]].push_back(j);
+    }
+  }
+  // window slots: own rows first, then imported rows (deduplicated, sorted)
+  std::vector<int32_t> slot_own(n, -1);
+  std::vector<std::unordered_map<int32_t, int32_t>> slot_imp((size_t)parts * nl);
+  out->wmax = out->rmax = 0;
+  for (int p = 0; p < parts; ++p)
+    for (int64_t l = 0; l < nl; ++l) {
+      auto& o = own[(size_t)p * nl + l];
+      for (size_t k = 0; k < o.size(); ++k) slot_own[o[k]] = (int32_t)k;
+      auto& im = imp[(size_t)p * nl + l];
+      std::sort(im.begin(), im.end());
+      im.erase(std::unique(im.begin(), im.end()), im.end());
+      auto& m = slot_imp[(size_t)p * nl + l];
+      for (size_t k = 0; k < im.size(); ++k) m[im[k]] = (int32_t)(o.size() + k);
+      out->rmax = std::max<int>(out->rmax, (int)((o.size() + 7) / 8 * 8));
+      out->wmax = std::max<int>(out->wmax, (int)(o.size() + im.size()));
+    }
+  if (out->rmax > cap_rows || out->wmax > cap_slots || (int64_t)W * out->wmax >= 32767) {
+    *why = "level too wide for the shared-memory windows";
+    return false;
+  }
+  const int wm = out->wmax;
+  // task order: part-major, level-major, row order
+  out->lvl_ptr.assign((size_t)parts * (nl + 1), 0);
+  out->task_row.clear();
+  for (int p = 0; p < parts; ++p) {
+    out->lvl_ptr[(size_t)p * (nl + 1)] = (int32_t)out->task_row.size();
+    for (int64_t l = 0; l < nl; ++l) {
+      auto& o = own[(size_t)p * nl + l];
+      out->task_row.insert(out->task_row.end(), o.begin(), o.end());
+      while (out->task_row.size() % 8) out->task_row.push_back(-1);  // 16-byte aligned blocks
+      out->lvl_ptr[(size_t)p * (nl + 1) + l + 1] = (int32_t)out->task_row.size();
+    }
+  }
+  const int64_t nt = (int64_t)out->task_row.size();
+  out->task_diag.assign(nt, 1.0);
+  out->ell_val.assign(nt * E, 0.0);
+  out->ell_code.assign(nt * E, (int16_t)-1);
+  for (int64_t k = 0; k < nt; ++k) {
+    const int32_t i = out->task_row[k];
+    if (i < 0) continue;
+    const int p = part[i];
+    int cnt = 0;
+    for (int64_t q = t.indptr[i]; q < t.indptr[i + 1]; ++q) {
+      const int32_t j = t.indices[q];
+      if (j == i) {
+        out->task_diag[k] = t.values[q];
+        continue;
+      }
+      const int32_t s = part[j] == p ? slot_own[j] : slot_imp[(size_t)p * nl + level[j]].at(j);
+      out->ell_code[k * E + cnt] = (int16_t)((level[j] % W) * wm + s);
+      out->ell_val[k * E + cnt] = t.values[q];
+      ++cnt;
+    }
+  }
+  // exports: owner p of row j pushes it to every part q that imports it
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> ex((size_t)parts * nl);
+  for (int q = 0; q < parts; ++q)
+    for (int64_t l = 0; l < nl; ++l)
+      for (auto& kv : slot_imp[(size_t)q * nl + l]) {
+        const int32_t j = kv.first;
+        const int32_t dst = (int32_t)((l % W) * wm + kv.second);
+        ex[(size_t)part[j] * nl + l].push_back({slot_own[j], (q << 16) | dst});
+      }
+  out->exp_ptr.assign((size_t)parts * (nl + 1), 0);
+  out->exp_src.clear();
+  out->exp_dst.clear();
+  out->emax = 0;
+  for (int p = 0; p < parts; ++p) {
+    out->exp_ptr[(size_t)p * (nl + 1)] = (int32_t)out->exp_src.size();
+    for (int64_t l = 0; l < nl; ++l) {
+      auto& e = ex[(size_t)p * nl + l];
+      std::sort(e.begin(), e.end());
+      for (auto& pr : e) {
+        out->exp_src.push_back(pr.first);
+        out->exp_dst.push_back(pr.second);
+      }
+      while (out->exp_src.size() % 4) {
+        out->exp_src.push_back(-1);
+        out->exp_dst.push_back(0);
+      }
+      out->emax = std::max<int>(out->emax, (int)((e.size() + 3) / 4 * 4));
+      out->exp_ptr[(size_t)p * (nl + 1) + l + 1] = (int32_t)out->exp_src.size();
+    }
   }
   return true;
 }

@@ -88,3 +88,34 @@ bool build_tile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t
                          int parts, int G, int R, TileSchedule* out, bool entry_major = false);
 
 }  // namespace bd
+
+namespace bd {
+
+// Cluster-wavefront schedule: P parts (one CTA each, one thread-block cluster),
+// all parts step through the global levels together.  Dependencies are read
+// from a ring of W level windows in shared memory: a part's own rows of a
+// level plus the rows of other parts it imports (pushed by their owners via
+// distributed shared memory).  Valid only if every dependency is at most W-1
+// levels back.
+struct ClusterSchedule {
+  int parts = 0, E = 0, W = 4;
+  int nlevels = 0;
+  int wmax = 0;        // window slots per level (own + imported), max over parts/levels
+  int rmax = 0;        // own rows per level, max over parts/levels
+  int emax = 0;        // export entries per level, max
+  std::vector<int32_t> lvl_ptr;   // parts*(nlevels+1): row offsets (task order, part-major)
+  std::vector<int32_t> task_row;  // ntasks
+  std::vector<double> task_diag;  // ntasks
+  std::vector<double> ell_val;    // ntasks*E
+  std::vector<int16_t> ell_code;  // ntasks*E: window index ((lvl%W)*wmax + slot), -1 padding
+  std::vector<int32_t> exp_ptr;   // parts*(nlevels+1)
+  std::vector<int32_t> exp_src;   // own slot (within the level window)
+  std::vector<int32_t> exp_dst;   // (dest part << 16) | dest window index
+};
+// Returns false if a dependency reaches further back than W-1 levels or the
+// windows/rows exceed the given caps.
+bool build_cluster_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& part,
+                            int parts, int E, int W, int cap_rows, int cap_slots,
+                            ClusterSchedule* out, std::string* why);
+
+}  // namespace bd
