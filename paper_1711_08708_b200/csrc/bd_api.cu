@@ -840,6 +840,24 @@ bd_status inner_solve(bd_inner* p, const Rhs& rhs, double* x_int, double* out, c
 // ---- operator -----------------------------------------------------------------
 bd_status launch_lambda(bd_system* s, const double* x, double* q, const Ctl& c, int with_dot) {
   bd_ctx* ctx = s->ctx;
+  const char* lv = getenv("BD_LAMBDA");
+  if (!(lv && lv[0] == '1')) {
+    // entries per row ~ nnz/n: 3D P1 ~15 -> 8 lanes x 2, 2D ~7 -> 4 lanes x 2
+    const double avg = s->n ? (double)s->S1->nnz / s->n : 1.0;
+    auto s1 = s->S1->dev();
+    auto si = s->Si->dev();
+    if (avg <= 8.0) {
+      const int grid = grid_for(ctx, s->n, dev::TPB / 4);
+      dev::k_lambda2<4, 2><<<grid, dev::TPB, 0, ctx->stream>>>(s1, si, x, q, s->mh, s->gamma,
+                                                              (int)s->n, (int)s->m, c, with_dot);
+    } else {
+      const int grid = grid_for(ctx, s->n, dev::TPB / 8);
+      dev::k_lambda2<8, 2><<<grid, dev::TPB, 0, ctx->stream>>>(s1, si, x, q, s->mh, s->gamma,
+                                                              (int)s->n, (int)s->m, c, with_dot);
+    }
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   const int G = s->S1->G;
   const int grid = grid_for(ctx, s->n, dev::TPB / G);
   auto s1 = s->S1->dev();
@@ -872,6 +890,19 @@ bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, c
 
 bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
   bd_ctx* ctx = p->sys->ctx;
+  {
+    const double avg = p->sys->m ? (double)p->sys->Si->nnz / p->sys->m : 1.0;
+    auto si2 = p->sys->Si->dev();
+    if (avg <= 8.0) {
+      dev::k_corr2<4, 2><<<grid_for(ctx, p->sys->m, dev::TPB / 4), dev::TPB, 0, ctx->stream>>>(
+          si2, s, p->corr, c, p->sys->n);
+    } else {
+      dev::k_corr2<8, 2><<<grid_for(ctx, p->sys->m, dev::TPB / 8), dev::TPB, 0, ctx->stream>>>(
+          si2, s, p->corr, c, p->sys->n);
+    }
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   const int G = p->sys->Si->G;
   const int grid = grid_for(ctx, p->sys->m, dev::TPB / G);
   auto si = p->sys->Si->dev();

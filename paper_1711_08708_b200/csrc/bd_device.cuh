@@ -361,6 +361,87 @@ __global__ void __launch_bounds__(TPB) k_lambda(Csr s1, Csr si, const double* __
   }
 }
 
+// Λ with K entries per lane: the S_1 and S_i entries of a row are loaded, and
+// their operands gathered, before any reduction (two memory round trips per
+// row instead of four).  Rows longer than G*K fall back to a loop.
+template <int G, int K>
+__global__ void __launch_bounds__(TPB) k_lambda2(Csr s1, Csr si, const double* __restrict__ x,
+                                                 double* __restrict__ q,
+                                                 const double* __restrict__ mh, double gamma,
+                                                 int n, int m, Ctl c, int with_dot) {
+  if (inactive(c)) return;
+  __shared__ double sm[32];
+  const int lane = threadIdx.x % G;
+  const int rpb = TPB / G;
+  const double* __restrict__ u = x;
+  const double* __restrict__ v = x + n;
+  double acc = 0.0;
+  for (int64_t base = (int64_t)blockIdx.x * rpb; base < n; base += (int64_t)gridDim.x * rpb) {
+    const int row = (int)(base + threadIdx.x / G);
+    const bool ok = row < n, okh = row < m;
+    int b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+    if (ok) {
+      b1 = s1.rowptr[row];
+      e1 = s1.rowptr[row + 1];
+    }
+    if (okh) {
+      b2 = si.rowptr[row];
+      e2 = si.rowptr[row + 1];
+    }
+    double a1[K], a2[K], x1[K], x2u[K], x2v[K];
+    int c1[K], c2[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const int k1 = b1 + lane + t * G, k2 = b2 + lane + t * G;
+      c1[t] = k1 < e1 ? s1.col[k1] : -1;
+      a1[t] = k1 < e1 ? s1.val[k1] : 0.0;
+      c2[t] = k2 < e2 ? si.col[k2] : -1;
+      a2[t] = k2 < e2 ? si.val[k2] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      x1[t] = c1[t] >= 0 ? __ldg(&u[c1[t]]) : 0.0;
+      x2u[t] = c2[t] >= 0 ? __ldg(&u[c2[t]]) : 0.0;
+      x2v[t] = c2[t] >= 0 ? __ldg(&v[c2[t]]) : 0.0;
+    }
+    double s_top = 0.0, su = 0.0, sv = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      s_top = fma(a1[t], x1[t], s_top);
+      su = fma(a2[t], x2u[t], su);
+      sv = fma(a2[t], x2v[t], sv);
+    }
+    for (int k1 = b1 + lane + K * G; k1 < e1; k1 += G) s_top = fma(s1.val[k1], __ldg(&u[s1.col[k1]]), s_top);
+    for (int k2 = b2 + lane + K * G; k2 < e2; k2 += G) {
+      const double a = si.val[k2];
+      const int j = si.col[k2];
+      su = fma(a, __ldg(&u[j]), su);
+      sv = fma(a, __ldg(&v[j]), sv);
+    }
+    s_top = group_sum<G>(s_top);
+    if (base < m) {  // block-uniform
+      su = group_sum<G>(su);
+      sv = group_sum<G>(sv);
+    }
+    if (lane == 0 && ok) {
+      double top = s_top;
+      if (okh) {
+        top = __dadd_rn(top, sv);
+        const double vi = v[row];
+        const double bot = __dadd_rn(__dadd_rn(su, sv), __dmul_rn(gamma, __dmul_rn(mh[row], vi)));
+        q[n + row] = bot;
+        acc = fma(vi, bot, acc);
+      }
+      q[row] = top;
+      acc = fma(u[row], top, acc);
+    }
+  }
+  if (with_dot) {
+    double vv[1] = {block_sum(acc, sm)};
+    reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_LAMBDA, FIN_DQ, 0, -1, 0, sm);
+  }
+}
+
 // r = b - q (warm start) or r = b; ||r||^2 and sum(r_u) (bd/krylov.py:74-85)
 __global__ void __launch_bounds__(TPB) k_init_res(const double* b, const double* q, double* r,
                                                   int64_t n, int64_t nm, Ctl c) {
@@ -1667,6 +1748,47 @@ __global__ void __launch_bounds__(TPB) k_corr(Csr si, const double* __restrict__
   }
   double v[1] = {block_sum(acc, sm)};
   reduce_tail<1>(c, v, gridDim.x, blockIdx.x, C_CORR, FIN_MEAN, S_MU2, S_C2, n, sm);
+}
+
+// k_corr with K entries per lane, loads issued before the reduction.
+template <int G, int K>
+__global__ void __launch_bounds__(TPB) k_corr2(Csr si, const double* __restrict__ s,
+                                               double* __restrict__ corr, Ctl c, int64_t n) {
+  if (inactive(c)) return;
+  __shared__ double sm[32];
+  const int lane = threadIdx.x % G;
+  const int rpb = TPB / G;
+  double acc = 0.0;
+  for (int64_t base = (int64_t)blockIdx.x * rpb; base < si.nrows; base += (int64_t)gridDim.x * rpb) {
+    const int64_t r = base + threadIdx.x / G;
+    const bool ok = r < si.nrows;
+    int b = 0, e = 0;
+    if (ok) {
+      b = si.rowptr[r];
+      e = si.rowptr[r + 1];
+    }
+    double a[K], xv[K];
+    int cc[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const int k = b + lane + t * G;
+      cc[t] = k < e ? si.col[k] : -1;
+      a[t] = k < e ? si.val[k] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < K; ++t) xv[t] = cc[t] >= 0 ? __ldg(&s[cc[t]]) : 0.0;
+    double v = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) v = fma(a[t], xv[t], v);
+    for (int k = b + lane + K * G; k < e; k += G) v = fma(si.val[k], __ldg(&s[si.col[k]]), v);
+    v = group_sum<G>(v);
+    if (ok && lane == 0) {
+      corr[r] = v;
+      acc += v;
+    }
+  }
+  double vv[1] = {block_sum(acc, sm)};
+  reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_CORR, FIN_MEAN, S_MU2, S_C2, n, sm);
 }
 
 // z_u = t - bulk(corr) with both recentrings applied on the fly
