@@ -119,6 +119,21 @@ struct DevCluster {
   }
 };
 
+struct DevDTile {
+  int* tile_row_ptr = nullptr;
+  int* tile_step_ptr = nullptr;
+  int* step_row = nullptr;
+  int* task_row = nullptr;
+  double* task_diag = nullptr;
+  int* ell_col = nullptr;
+  double* ell_val = nullptr;
+  int ntiles = 0, tmax = 0, grid = 0, threads = 64;
+  dev::DTileDev dev() const {
+    return dev::DTileDev{tile_row_ptr, tile_step_ptr, step_row, task_row, task_diag,
+                         ell_col,      ell_val,       ntiles,   tmax};
+  }
+};
+
 struct DevSuper {
   int* sn_start = nullptr;
   int* sn_size = nullptr;
@@ -137,6 +152,8 @@ struct bd_inner {
   DevSuper SL, SU;
   bool cluster = false;
   DevCluster CL, CU;
+  bool dtile = false;
+  DevDTile DL, DU;
   double* rtmp = nullptr;
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
@@ -687,6 +704,70 @@ bd_status launch_cluster(bd_inner* p, const DevCluster& cd, const Rhs& rhs, doub
   return BD_OK;
 }
 
+bd_status upload_dtile(bd_ctx* ctx, const DTileSchedule& ds, DevDTile* out) {
+  CK(ctx, upload_vec(&out->tile_row_ptr, ds.tile_row_ptr));
+  CK(ctx, upload_vec(&out->tile_step_ptr, ds.tile_step_ptr));
+  CK(ctx, upload_vec(&out->step_row, ds.step_row));
+  CK(ctx, upload_vec(&out->task_row, ds.task_row));
+  CK(ctx, upload_vec(&out->task_diag, ds.task_diag));
+  CK(ctx, upload_vec(&out->ell_col, ds.ell_col));
+  CK(ctx, upload_vec(&out->ell_val, ds.ell_val));
+  out->ntiles = (int)ds.tile_row_ptr.size() - 1;
+  out->tmax = ds.tmax;
+  out->threads = std::max(32, (ds.tmax + 31) / 32 * 32);  // one row per thread (<= 256)
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_dtile<8, dev::RhsGather>,
+                                                out->threads, 0);
+  out->grid = (int)std::min<int64_t>(out->ntiles, (int64_t)ctx->nsm * std::max(1, per_sm));
+  return BD_OK;
+}
+
+void free_dtile(DevDTile* d) {
+  cudaFree(d->tile_row_ptr);
+  cudaFree(d->tile_step_ptr);
+  cudaFree(d->step_row);
+  cudaFree(d->task_row);
+  cudaFree(d->task_diag);
+  cudaFree(d->ell_col);
+  cudaFree(d->ell_val);
+}
+
+bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
+                      const double* coords, int dim) {
+  bd_ctx* ctx = p->ctx;
+  const int target = getenv("BD_DTILE_ROWS") ? atoi(getenv("BD_DTILE_ROWS")) : 64;
+  const int ntiles = (int)std::max<int64_t>(1, lower.n / target);
+  std::vector<int32_t> tile;
+  if (coords && dim > 0)
+    partition_coords(lower.n, dim, coords, ntiles, &tile);
+  else
+    partition_rows(lower, ntiles, &tile);
+  int E = 4;
+  for (int64_t i = 0; i < lower.n; ++i)
+    while (E < lower.indptr[i + 1] - lower.indptr[i] - 1) E <<= 1;
+  for (int64_t i = 0; i < upper.n; ++i)
+    while (E < upper.indptr[i + 1] - upper.indptr[i] - 1) E <<= 1;
+  if (E > 8) return BD_OK;
+  DTileSchedule dl, du;
+  std::string why;
+  bool ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
+            build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  if (ok && (std::max(dl.tmax, du.tmax) > dev::DT_MAX_ROWS ||
+             std::max(dl.smax, du.smax) > dev::DT_MAX_STEPS)) {
+    ok = false;
+    why = "tile too large";
+  }
+  if (getenv("BD_DEBUG"))
+    std::fprintf(stderr, "[bd] dtile n=%lld tiles=%d: %s (tmax %d, smax %d)\n", (long long)lower.n,
+                 ntiles, ok ? "ok" : why.c_str(), dl.tmax, dl.smax);
+  if (!ok) return BD_OK;
+  TRY(upload_dtile(ctx, dl, &p->DL));
+  TRY(upload_dtile(ctx, du, &p->DU));
+  p->G = E;
+  p->dtile = true;
+  return BD_OK;
+}
+
 template <int G, class Rhs>
 bd_status launch_tiled(bd_inner* p, const DevTile& t, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr, int fin, int slot, int slot2, int64_t nmean) {
@@ -743,6 +824,29 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->dtile) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    if (p->G == 4)
+      dev::k_trsv_dtile<4, Rhs><<<p->DL.grid, p->DL.threads, 0, st>>>(p->DL.dev(), rhs, p->y_int, c,
+                                                                       ctr0, ctr0 + 1);
+    else
+      dev::k_trsv_dtile<8, Rhs><<<p->DL.grid, p->DL.threads, 0, st>>>(p->DL.dev(), rhs, p->y_int, c,
+                                                                       ctr0, ctr0 + 1);
+    LAUNCHED(ctx);
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    if (p->G == 4)
+      dev::k_trsv_dtile<4, dev::RhsGather><<<p->DU.grid, p->DU.threads, 0, st>>>(
+          p->DU.dev(), dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3);
+    else
+      dev::k_trsv_dtile<8, dev::RhsGather><<<p->DU.grid, p->DU.threads, 0, st>>>(
+          p->DU.dev(), dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3);
+    LAUNCHED(ctx);
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->cluster) {
@@ -1363,14 +1467,17 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   }
   if (st == BD_OK && kind == BD_INNER_IC0) {
     const char* mode = getenv("BD_TRSV");
-    const std::string m = mode ? mode : "persist";
+    const std::string m = mode ? mode : "dtile";
     if (m == "cluster") {
       st = setup_cluster(p, lower, upper, coords, dim);
+    }
+    if (m == "dtile") {
+      st = setup_dtile(p, lower, upper, coords, dim);
     }
     if (m == "tiled" || m == "rows") {
       p->rows_mode = (m == "rows");
       st = setup_tiles(p, lower, upper, coords, dim);
-    } else if (m == "persist" || (m == "cluster" && !p->cluster)) {
+    } else if (m == "persist" || (m == "cluster" && !p->cluster) || (m == "dtile" && !p->dtile)) {
       int64_t maxoff = 0;
       for (int64_t i = 0; i < n; ++i)
         maxoff = std::max<int64_t>(maxoff, lower.indptr[i + 1] - lower.indptr[i] - 1);
@@ -1419,6 +1526,8 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_super(&p->SU);
   free_cluster(&p->CL);
   free_cluster(&p->CU);
+  free_dtile(&p->DL);
+  free_dtile(&p->DU);
   cudaFree(p->rtmp);
   cudaFree(p->perm);
   cudaFree(p->inv);

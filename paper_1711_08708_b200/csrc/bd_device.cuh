@@ -518,6 +518,7 @@ struct RhsSchur {
       e = si.rowptr[i + 1];
     }
     double s = 0.0;
+#pragma unroll 4
     for (int k = b + lane; k < e; k += G) {
       const double t = __dadd_rn(__dsub_rn(__ldg(&traw[si.col[k]]), mt), c1);
       s = fma(si.val[k], t, s);
@@ -1302,6 +1303,111 @@ __global__ void __launch_bounds__(1024, 1) k_trsv_cluster(ClusterDev S, Rhs rhs,
     }
   }
   cp_async_wait<0>();
+}
+
+// ---- dynamic-tile triangular solve --------------------------------------------------
+// Rows are grouped into small tiles (~64 rows, a 4x4x4 box on the Kuhn grid)
+// listed in a topological order of the tile DAG.  A persistent grid grabs
+// tiles in that order (a tile only waits on earlier tiles, all owned by
+// running blocks); inside a tile one thread owns one row and the tile steps
+// through its own few levels with a block barrier, reading same-tile
+// dependencies from shared memory and polling only cross-tile ones.
+struct DTileDev {
+  const int* tile_row_ptr;
+  const int* tile_step_ptr;
+  const int* step_row;
+  const int* task_row;
+  const double* task_diag;
+  const int* ell_col;
+  const double* ell_val;
+  int ntiles;
+  int tmax;
+};
+constexpr int DT_MAX_ROWS = 256;
+constexpr int DT_MAX_STEPS = 96;
+
+template <int E, class Rhs, int H = 1>
+__global__ void __launch_bounds__(256) k_trsv_dtile(DTileDev T, Rhs rhs, double* __restrict__ xg,
+                                                    Ctl c, int ctr_task, int ctr_done) {
+  if (inactive(c)) return;
+  __shared__ double xs[DT_MAX_ROWS + 1];
+  __shared__ int steps_s[DT_MAX_STEPS + 1];
+  __shared__ int task_s;
+  __shared__ int last_s;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (;;) {
+    if (tid == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+    __syncthreads();
+    const int t = task_s;
+    if (t >= T.ntiles) break;
+    const int r0 = T.tile_row_ptr[t], nr = T.tile_row_ptr[t + 1] - r0;
+    const int s0 = T.tile_step_ptr[t], ns = T.tile_step_ptr[t + 1] - s0;
+    for (int k = tid; k < ns; k += nth) steps_s[k] = T.step_row[s0 + k];
+    if (tid == 0) {
+      steps_s[ns] = nr;
+      xs[T.tmax] = 0.0;
+    }
+    // this thread's rows (tiles of up to H*nth rows: k = tid, tid + nth, ...)
+    int row[H], cl[H][E];
+    double dg[H], vl[H][E], b[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int k = tid + h * nth;
+      const bool ok = k < nr;
+      row[h] = ok ? T.task_row[r0 + k] : -1;
+      dg[h] = ok ? T.task_diag[r0 + k] : 1.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        cl[h][e] = ok ? T.ell_col[(int64_t)(r0 + k) * E + e] : -(T.tmax + 1);
+        vl[h][e] = ok ? T.ell_val[(int64_t)(r0 + k) * E + e] : 0.0;
+      }
+      b[h] = rhs.template eval<1>(row[h], 0);
+    }
+    __syncthreads();
+    for (int st = 0; st < ns; ++st) {
+      const int a = steps_s[st], e_ = steps_s[st + 1];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int k = tid + h * nth;
+        if (k >= a && k < e_) {
+          double xv[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int code = cl[h][e];
+            xv[e] = code < 0 ? xs[-code - 1] : ld_relaxed_if(&xg[code < 0 ? 0 : code], code >= 0);
+          }
+          bool late = false;
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            late |= (cl[h][e] >= 0) && (__double_as_longlong(xv[e]) == SENTINEL);
+          if (late) {
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              if (cl[h][e] >= 0 && __double_as_longlong(xv[e]) == SENTINEL)
+                xv[e] = spin_load(&xg[cl[h][e]]);
+          }
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc = fma(vl[h][e], xv[e], acc);
+          const double v = __ddiv_rn(__dsub_rn(b[h], acc), dg[h]);
+          xs[k] = v;
+          publish(&xg[row[h]], v);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && tid == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
 }
 
 // ---- persistent sync-free triangular solve ----------------------------------

@@ -791,3 +791,102 @@ bool build_cluster_schedule(const HostCsr& t, bool lower, const std::vector<int3
 }
 
 }  // namespace bd
+
+// ---------------------------------------------------------------------------
+#include <queue>
+namespace bd {
+
+bool build_dtile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& tile,
+                          int ntiles, int E, DTileSchedule* out, std::string* why) {
+  const int64_t n = t.n;
+  std::vector<int32_t> level;
+  row_levels(t, lower, &level);
+  std::vector<std::vector<int32_t>> rows(ntiles);
+  for (int64_t i = 0; i < n; ++i) rows[tile[i]].push_back((int32_t)i);
+  // tile DAG (edges from dependency tiles) and min level per tile
+  std::vector<int32_t> minlv(ntiles, INT32_MAX), indeg(ntiles, 0);
+  std::vector<std::vector<int32_t>> succ(ntiles);
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t ti = tile[i];
+    minlv[ti] = std::min(minlv[ti], level[i]);
+    int cnt = 0;
+    for (int64_t q = t.indptr[i]; q < t.indptr[i + 1]; ++q) {
+      const int32_t j = t.indices[q];
+      if (j == i) continue;
+      if (++cnt > E) {
+        *why = "row longer than the ELL width";
+        return false;
+      }
+      const int32_t tj = tile[j];
+      if (tj != ti) succ[tj].push_back(ti);
+    }
+  }
+  for (auto& s : succ) {
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    for (int32_t v : s) indeg[v]++;
+  }
+  // priority topological order: smallest min level first, then tile id
+  using Key = std::pair<int32_t, int32_t>;
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> pq;
+  for (int32_t v = 0; v < ntiles; ++v)
+    if (indeg[v] == 0) pq.push({minlv[v], v});
+  std::vector<int32_t> order;
+  order.reserve(ntiles);
+  while (!pq.empty()) {
+    const int32_t v = pq.top().second;
+    pq.pop();
+    order.push_back(v);
+    for (int32_t w : succ[v])
+      if (--indeg[w] == 0) pq.push({minlv[w], w});
+  }
+  if ((int)order.size() != ntiles) {
+    *why = "tile graph has a cycle";
+    return false;
+  }
+  out->E = E;
+  out->tmax = out->smax = 0;
+  out->tile_row_ptr.assign(1, 0);
+  out->tile_step_ptr.assign(1, 0);
+  out->step_row.clear();
+  out->task_row.clear();
+  std::vector<int32_t> slot(n, -1);
+  for (int32_t v : order) {
+    auto& r = rows[v];
+    std::stable_sort(r.begin(), r.end(),
+                     [&](int32_t a, int32_t b) { return level[a] < level[b]; });
+    for (size_t k = 0; k < r.size(); ++k) {
+      slot[r[k]] = (int32_t)k;
+      if (k == 0 || level[r[k]] != level[r[k - 1]]) out->step_row.push_back((int32_t)k);
+    }
+    out->task_row.insert(out->task_row.end(), r.begin(), r.end());
+    out->tile_row_ptr.push_back((int32_t)out->task_row.size());
+    out->tile_step_ptr.push_back((int32_t)out->step_row.size());
+    out->tmax = std::max<int>(out->tmax, (int)r.size());
+    out->smax = std::max<int>(out->smax, out->tile_step_ptr.back() -
+                                             out->tile_step_ptr[out->tile_step_ptr.size() - 2]);
+  }
+  const int64_t nt = (int64_t)out->task_row.size();
+  out->task_diag.assign(nt, 1.0);
+  out->ell_col.assign(nt * E, 0);
+  out->ell_val.assign(nt * E, 0.0);
+  const int32_t zero = -(out->tmax + 1);  // zero slot of every tile
+  for (int64_t k = 0; k < nt; ++k) {
+    const int32_t i = out->task_row[k];
+    int cnt = 0;
+    for (int64_t q = t.indptr[i]; q < t.indptr[i + 1]; ++q) {
+      const int32_t j = t.indices[q];
+      if (j == i) {
+        out->task_diag[k] = t.values[q];
+        continue;
+      }
+      out->ell_col[k * E + cnt] = tile[j] == tile[i] ? -(slot[j] + 1) : j;
+      out->ell_val[k * E + cnt] = t.values[q];
+      ++cnt;
+    }
+    for (; cnt < E; ++cnt) out->ell_col[k * E + cnt] = zero;
+  }
+  return true;
+}
+
+}  // namespace bd

@@ -119,3 +119,25 @@ bool build_cluster_schedule(const HostCsr& t, bool lower, const std::vector<int3
                             ClusterSchedule* out, std::string* why);
 
 }  // namespace bd
+
+namespace bd {
+
+// Dynamic-tile schedule: rows grouped into small tiles (coordinate or graph
+// bisection, ~tile_rows each), tiles listed in a priority topological order of
+// the tile DAG (priority = lowest row level), each tile's rows sorted by level
+// into steps.  ELL entries: col >= 0 row of another tile (polled), col < 0 is
+// -(slot+1) of a row of the same tile, padding = zero slot.
+struct DTileSchedule {
+  int E = 0, tmax = 0, smax = 0;
+  std::vector<int32_t> tile_row_ptr;   // ntiles+1 (task order)
+  std::vector<int32_t> tile_step_ptr;  // ntiles+1 into step_row
+  std::vector<int32_t> step_row;       // per step: first row offset within its tile
+  std::vector<int32_t> task_row;
+  std::vector<double> task_diag;
+  std::vector<int32_t> ell_col;        // ntasks*E
+  std::vector<double> ell_val;
+};
+bool build_dtile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& tile,
+                          int ntiles, int E, DTileSchedule* out, std::string* why);
+
+}  // namespace bd
