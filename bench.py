@@ -261,7 +261,8 @@ def run_native(args, rank, world, local_rank):
     ncu_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(ncu_path):
         with open(ncu_path) as fh:
-            traffic = json.load(fh).get(f"{wl.name}_{wl.inner}_bulk_solve_bytes")
+            traffic = json.load(fh).get(
+                f"{wl.name}_{wl.inner}_{os.environ.get('BD_TRSV', 'dtile')}_bulk_solve_bytes")
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -286,7 +287,8 @@ def run_native(args, rank, world, local_rank):
                     "wall_s": round(wall_e2e, 3)},
             "roofline": {"bound": "hbm",
                          "kernel": ("bulk inner solve pair: forward + backward triangular pass "
-                                    "(k_trsv_persist, P_1 block)") if wl.inner != "jacobi" else "jacobi",
+                                    f"(k_trsv_{os.environ.get('BD_TRSV', 'dtile')}, P_1 block)")
+                                   if wl.inner != "jacobi" else "jacobi",
                          "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
