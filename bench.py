@@ -309,6 +309,85 @@ def run_native(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def weak_cells(base, world):
+    """Refine the base slab so every GPU keeps a base-sized part: double the
+    axis with the most cells per rank first (8 GPUs on (128,128,64) -> the
+    BASELINE config-3 grid (256,256,128))."""
+    cells = list(base)
+    k = 1
+    while k * 2 <= world:
+        ax = min(range(3), key=lambda a: (cells[a] // base[a], a))
+        cells[ax] *= 2
+        k *= 2
+    if world != k:
+        cells[0] = cells[0] * world // k
+    return tuple(cells)
+
+
+def run_sharded(args, rank, world, local_rank):
+    """Mesh partitioned across the GPUs (RCB), NCCL halo exchange + allreduce,
+    block-Jacobi inner solves (paper_1711_08708_b200.distributed).  Weak
+    scaling: the slab is refined with N so each GPU keeps a cfg2-sized part."""
+    import torch
+    import torch.distributed as dist
+    from paper_1711_08708_b200 import _lib, configs
+    from paper_1711_08708_b200 import distributed as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = _lib.Context(local_rank)
+    _lib.Context._default = ctx
+    cells = weak_cells((128, 128, 64), world)
+    wl = configs.cfg2(cells, inner=args.inner or "ic0", name="cfg3" if cells == (256, 256, 128) else "cfg2")
+    t0 = time.perf_counter()
+    part = D.rcb_partition(wl.mesh.vertices, world)
+    sim = D.DistributedSimulation(wl, part, rank, world, dist, dev)
+    t_setup = time.perf_counter() - t0
+    log(f"[rank {rank}] sharded {cells}: n_own={sim.lp.n_own} ghosts={sim.lp.ghosts.size} "
+        f"setup {t_setup:.1f}s")
+    state = sim.resting()
+    for _ in range(args.warmup):
+        state, _ = sim.step(state)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = ctx.launches()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        state, st = sim.step(state)
+        iters.append(st["iterations"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    n, m = wl.n, wl.n_heart
+    base_dof = 2 * (129 * 129 * 65)
+    steps_s = args.steps / (ms / 1e3)
+    value = steps_s * (n + m) / base_dof  # cfg2-equivalent time steps per second (aggregate)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic structured mesh)",
+            "config": {"workload": f"{wl.name} slab {cells[0]}x{cells[1]}x{cells[2]} sharded "
+                                   f"(RCB, NCCL halo + allreduce, block-Jacobi {wl.inner})",
+                       "dof": n + m, "raw_steps_per_s": round(steps_s, 4),
+                       "value_definition": "steps/s x dof / dof(cfg2): cfg2-equivalent steps/s",
+                       "pcg_iters_per_step": round(float(np.mean(iters)), 2),
+                       "parallelism": f"mesh partition x{world}"},
+            "gpu_launches": int(ctx.launches() - launches0), "clocks": clk,
+            "setup_s": round(t_setup, 1)}), flush=True)
+
+
 def cpu_baseline(sysm, km, wl, iters_per_step, n_iter):
     """Oracle port, 1 thread: time a bounded number of PCG iterations of the
     same workload's first step and extrapolate with the iterations per step."""
@@ -434,6 +513,10 @@ def main():
     ap.add_argument("--inner", default=None)
     ap.add_argument("--cpu-iters", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default=os.environ.get("BD_BENCH_MODE", "replicas"),
+                    choices=["replicas", "sharded"],
+                    help="N>1: independent replicas of cfg2 per GPU, or the mesh sharded "
+                         "across GPUs (weak scaling, 8 GPUs = config 3)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -446,6 +529,17 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.mode == "sharded":
+        if world == 1:
+            import torch
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        run_sharded(args, rank, world, local_rank)
+        import torch.distributed as dist
+        dist.destroy_process_group()
+        return
     run_native(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -175,6 +175,13 @@ bd_status bd_membrane_rhs(bd_system* s, const double* v, const double* w,
                           double amplitude, double chi, double v_rest, double v_span,
                           double tau_in, double tau_out, double c_m, double* rhs,
                           double* ion);
+/* Same without a bd_system (sharded ranks): n, m, heart_mass (device, m) and
+ * gamma given explicitly. */
+bd_status bd_membrane_rhs_raw(bd_ctx* ctx, int64_t n, int64_t m, const double* heart_mass,
+                              double gamma, const double* v, const double* w,
+                              const uint64_t* site_mask, uint64_t active_sites, double amplitude,
+                              double chi, double v_rest, double v_span, double tau_in,
+                              double tau_out, double c_m, double* rhs, double* ion);
 /* w_new = clip(w + dt * (u < u_gate ? (1-w)/tau_open : -w/tau_close), 0, 1)
  * with u = (v - v_rest)/v_span (update_gate, bd/ionic.py:55-68); device m. */
 bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double* w,

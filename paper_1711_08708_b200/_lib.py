@@ -79,6 +79,8 @@ SIGNATURES = [
     ("bd_launch_count", _i64, [_vp]),
     ("bd_membrane_rhs", _i32, [_vp, _vp, _vp, _vp, C.c_uint64, _dbl, _dbl, _dbl, _dbl, _dbl,
                                _dbl, _dbl, _vp, _vp]),
+    ("bd_membrane_rhs_raw", _i32, [_vp, _i64, _i64, _vp, _dbl, _vp, _vp, _vp, C.c_uint64, _dbl,
+                                   _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, _vp]),
     ("bd_membrane_gate", _i32, [_vp, _i64, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _vp]),
 ]
 

@@ -1895,6 +1895,20 @@ bd_status bd_membrane_rhs(bd_system* s, const double* v, const double* w, const 
   return BD_OK;
 }
 
+bd_status bd_membrane_rhs_raw(bd_ctx* ctx, int64_t n, int64_t m, const double* heart_mass,
+                              double gamma, const double* v, const double* w,
+                              const uint64_t* site_mask, uint64_t active_sites, double amplitude,
+                              double chi, double v_rest, double v_span, double tau_in,
+                              double tau_out, double c_m, double* rhs, double* ion) {
+  if (!ctx || !heart_mass || !v || !w || !rhs) return BD_EINVAL;
+  Scope sc(ctx);
+  dev::k_membrane_rhs<<<grid_for(ctx, n + m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      n, m, v, w, site_mask, active_sites, amplitude, chi, gamma, heart_mass, v_rest, v_span,
+      tau_in, tau_out, c_m, rhs, ion);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
 bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double* w, double dt,
                            double v_rest, double v_span, double tau_open, double tau_close,
                            double u_gate, double* w_new) {

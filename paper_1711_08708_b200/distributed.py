@@ -360,3 +360,187 @@ class NativeBackend:
 
     def inner_apply(self, h, y):
         return h.apply_inverse(y.contiguous())
+
+
+# ---- per-rank setup without global matrices (large meshes) --------------------------
+def _rows_csr(mesh, field, space, owned_rows, n_cols):
+    """CSR (len(owned_rows) × n_cols, global column ids) of the stiffness rows
+    of `owned_rows`, assembled from the elements that touch them only
+    (same element matrices as assembly.assemble_stiffness)."""
+    from .assembly import _grads_volumes, _select
+    elements, tags, n = _select(mesh, space)
+    pos = -np.ones(n, dtype=np.int64)
+    pos[owned_rows] = np.arange(owned_rows.size)
+    touch = (pos[elements] >= 0).any(axis=1)
+    el, tg = elements[touch], tags[touch]
+    if el.shape[0] == 0:
+        return sp.csr_matrix((owned_rows.size, n_cols))
+    grads, vols = _grads_volumes(mesh.vertices, el, mesh.dim)
+    sigma = field.evaluate_batch(mesh.vertices[el].mean(axis=1), tg)
+    local = np.einsum("eid,edk,ejk->eij", grads, sigma, grads)
+    local = 0.5 * (local + local.transpose(0, 2, 1))
+    local *= vols[:, None, None]
+    arity = mesh.dim + 1
+    rows = np.repeat(el, arity, axis=1).ravel()
+    cols = np.tile(el, (1, arity)).ravel()
+    keep = pos[rows] >= 0
+    out = sp.coo_matrix((local.ravel()[keep], (pos[rows[keep]], cols[keep])),
+                        shape=(owned_rows.size, n_cols)).tocsr()
+    out.sum_duplicates()
+    out.sort_indices()
+    return out
+
+
+def _rows_mass(mesh, space, owned_rows):
+    from .assembly import _select
+    import math
+    elements, _, n = _select(mesh, space)
+    pos = -np.ones(n, dtype=np.int64)
+    pos[owned_rows] = np.arange(owned_rows.size)
+    touch = (pos[elements] >= 0).any(axis=1)
+    el = elements[touch]
+    coords = mesh.vertices[el]
+    det = np.linalg.det(coords[:, 1:, :] - coords[:, :1, :])
+    share = det / math.factorial(mesh.dim) / (mesh.dim + 1)
+    out = np.zeros(owned_rows.size)
+    for k in range(mesh.dim + 1):
+        p = pos[el[:, k]]
+        ok = p >= 0
+        np.add.at(out, p[ok], share[ok])
+    return out
+
+
+def ghost_sets(mesh, part: np.ndarray, nprocs: int):
+    """Ghost vertices of every rank from the element connectivity: vertices
+    of other ranks sharing an element with an owned vertex (heart first,
+    then torso, each ascending — the order build_local uses)."""
+    el = mesh.elements
+    m = mesh.heart_vertex_count
+    pe = part[el]
+    out = []
+    for r in range(nprocs):
+        touch = (pe == r).any(axis=1)
+        v = np.unique(el[touch])
+        g = v[part[v] != r]
+        out.append(np.concatenate([g[g < m], g[g >= m]]))
+    return out
+
+
+def build_local_from_mesh(mesh, params, fibers, dt, part: np.ndarray, rank: int, nprocs: int,
+                          comm_allreduce=None) -> "LocalProblem":
+    """The rank-local problem assembled from the elements touching the owned
+    vertices only.  beta (mean diagonal of S_1, bd/precond.py:79-81) needs a
+    global sum: comm_allreduce(list) -> list (None: single process)."""
+    from .assembly import Space
+    from .conductivity import TensorField
+    from .system import gamma as gamma_fn
+    n, m, d = mesh.vertex_count, mesh.heart_vertex_count, mesh.dim
+    gam = gamma_fn(params.chi, params.c_m, dt)
+    own = np.flatnonzero(part == rank)
+    owned = np.concatenate([own[own < m], own[own >= m]])
+    ghosts_all = ghost_sets(mesh, part, nprocs)
+    ghosts = ghosts_all[rank]
+    m_own, m_ghost = int((owned < m).sum()), int((ghosts < m).sum())
+    S1 = _rows_csr(mesh, TensorField(params, d, "bar1", fibers), Space.FULL, owned, n)
+    Si = _rows_csr(mesh, TensorField(params, d, "intra", fibers), Space.HEART_ONLY, owned[:m_own], m)
+    Sm = _rows_csr(mesh, TensorField(params, d, "mono", fibers), Space.HEART_ONLY, owned[:m_own], m)
+    mass = _rows_mass(mesh, Space.FULL, owned)
+    mh = _rows_mass(mesh, Space.HEART_ONLY, owned[:m_own])
+    diag_sum = float(S1[np.arange(owned.size), owned].sum())
+    tot = comm_allreduce([diag_sum]) if comm_allreduce else [diag_sum]
+    beta = tot[0] / n
+    ext = np.concatenate([owned, ghosts])
+    g2l = -np.ones(n, dtype=np.int64)
+    g2l[ext] = np.arange(ext.size)
+    s1 = S1[:, ext].tocsr()
+    hext = np.concatenate([owned[:m_own], ghosts[:m_ghost]])
+    hmap = -np.ones(m, dtype=np.int64)
+    hmap[hext] = np.arange(hext.size)
+    si = Si[:, hext].tocsr()
+    # block-Jacobi diagonal blocks: grounded S_1 (beta on global vertex 0) and K_m
+    gb = S1[:, owned].tocsr()
+    if part[0] == rank:
+        k0 = int(np.flatnonzero(owned == 0)[0])
+        bump = sp.csr_matrix(([beta], ([k0], [k0])), shape=gb.shape)
+        gb = (gb + bump).tocsr()
+    km = (Sm[:, owned[:m_own]] + gam * sp.diags(mh)).tocsr()
+    for a in (s1, si, gb, km):
+        a.sum_duplicates()
+        a.sort_indices()
+    lp = LocalProblem(rank, nprocs, n, m, owned, ghosts, owned.size, m_own, m_ghost, s1, si,
+                      mass, mh, float(gam), gb, km)
+    for q in range(nprocs):
+        if q == rank:
+            continue
+        need = ghosts_all[q][part[ghosts_all[q]] == rank]
+        if need.size:
+            lp.send[q] = g2l[need]
+            hm = need < m
+            if hm.any():
+                lp.send_heart[q] = g2l[need[hm]]
+        mine = ghosts[part[ghosts] == q]
+        if mine.size:
+            lp.recv[q] = g2l[mine] - owned.size
+            hm = mine < m
+            if hm.any():
+                lp.recv_heart[q] = g2l[mine[hm]] - owned.size
+    lp.beta = beta
+    return lp
+
+
+class DistributedSimulation:
+    """Sharded time loop: membrane RHS and gate on the owned heart vertices
+    (sm_100a kernels), the coupled solve by distributed_pcg."""
+
+    def __init__(self, wl, part: np.ndarray, rank: int, nprocs: int, dist, device, inner=None):
+        import torch
+
+        from . import _lib
+        from .ionic import site_masks
+
+        self.wl = wl
+        self.comm = Comm(dist, device)
+        self.lp = build_local_from_mesh(wl.mesh, wl.params, wl.fibers, wl.dt, part, rank, nprocs,
+                                        comm_allreduce=self.comm.allreduce)
+        self.backend = NativeBackend()
+        self.dsys = DistributedSystem(self.lp, self.comm, self.backend)
+        self.prec = DistributedBlockLU(self.dsys, inner or wl.inner, self.lp.beta)
+        lp = self.lp
+        pts = wl.mesh.vertices[lp.owned[: lp.m_own]]
+        masks = site_masks(pts, wl.protocol) if wl.protocol.sites else None
+        self.mask = (torch.as_tensor(masks.view(np.int64)).to(device) if masks is not None
+                     else None)
+        self.mh = torch.as_tensor(lp.heart_mass, device=device)
+        self.ctx = _lib.Context.default()
+        self._lib = _lib
+        self.device = device
+
+    def resting(self):
+        import torch
+        lp, ion = self.lp, self.wl.ionic
+        return (torch.zeros(lp.n_own, dtype=torch.float64, device=self.device),
+                torch.full((lp.m_own,), ion.v_rest, dtype=torch.float64, device=self.device),
+                torch.ones(lp.m_own, dtype=torch.float64, device=self.device), 0.0)
+
+    def step(self, state):
+        """(u, v, w, t) -> new state, stats (bd/simulate.py:134-170, sharded)."""
+        import torch
+        from .ionic import active_sites
+        u, v, w, t = state
+        lp, wl, L = self.lp, self.wl, self._lib
+        ion = wl.ionic
+        rhs = torch.empty(lp.n_own + lp.m_own, dtype=torch.float64, device=self.device)
+        L.check(L.lib().bd_membrane_rhs_raw(
+            self.ctx.handle, lp.n_own, lp.m_own, L.ptr(self.mh), lp.gamma, L.ptr(v), L.ptr(w),
+            L.ptr(self.mask), int(active_sites(t, wl.protocol)), float(wl.protocol.amplitude),
+            float(wl.params.chi), float(ion.v_rest), float(ion.v_span), float(ion.tau_in),
+            float(ion.tau_out), float(wl.params.c_m), L.ptr(rhs), None), self.ctx.handle)
+        x, st = distributed_pcg(self.dsys, self.prec, rhs, tol=wl.tol, max_iter=20000,
+                                x0=torch.cat([u, v]))
+        v_new = x[lp.n_own:].contiguous()
+        w_new = torch.empty_like(w)
+        L.check(L.lib().bd_membrane_gate(
+            self.ctx.handle, lp.m_own, L.ptr(v_new), L.ptr(w), float(wl.dt), float(ion.v_rest),
+            float(ion.v_span), float(ion.tau_open), float(ion.tau_close), float(ion.u_gate),
+            L.ptr(w_new)), self.ctx.handle)
+        return (x[: lp.n_own].contiguous(), v_new, w_new, t + wl.dt), st

@@ -130,3 +130,37 @@ def test_distributed_pcg_gloo_world2(inner, tmp_path):
         assert abs(iters[0] - int(g["sanity_jacobi_iters"])) <= 2
     else:  # block-Jacobi IC(0) changes the preconditioner: report, bounded
         assert iters[0] <= 3 * int(g["sanity_ic0_iters"])
+
+
+def test_local_assembly_matches_global():
+    """Per-rank assembly from the touching elements reproduces the rows of the
+    global matrices and the global halo plan."""
+    from paper_1711_08708_b200 import configs
+    from paper_1711_08708_b200.precond import build_monodomain_matrix, regularize_stiffness
+    from paper_1711_08708_b200.system import BidomainSystem
+    wl = configs.cfg1(32)  # heart-in-torso: heart-first numbering, torso and heart ghosts
+    sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
+    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+    reg = regularize_stiffness(sysm.stiff_total)
+    part = D.rcb_partition(wl.mesh.vertices, 3)
+    for r in range(3):
+        ref = D.build_local(sysm.stiff_total, sysm.stiff_intra, sysm.mass_diag,
+                            sysm.heart_mass_diag, sysm.gamma, reg.grounded(), km, part, r, 3)
+        tot = float(sysm.stiff_total.diagonal().sum())  # stands in for the all_reduce
+        loc = D.build_local_from_mesh(wl.mesh, wl.params, wl.fibers, wl.dt, part, r, 3,
+                                      comm_allreduce=lambda v: [tot])
+        assert np.array_equal(ref.owned, loc.owned) and np.array_equal(ref.ghosts, loc.ghosts)
+        assert loc.beta == pytest.approx(reg.beta, rel=1e-14)
+        for a, b in ((ref.S1, loc.S1), (ref.Si, loc.Si), (ref.bulk_block, loc.bulk_block),
+                     (ref.schur_block, loc.schur_block)):
+            assert a.shape == b.shape
+            np.testing.assert_allclose(a.toarray(), b.toarray(), rtol=0,
+                                       atol=1e-13 * max(1.0, np.abs(a.data).max()))
+        np.testing.assert_allclose(loc.mass, ref.mass, rtol=1e-14)
+        np.testing.assert_allclose(loc.heart_mass, ref.heart_mass, rtol=1e-14)
+        for q in ref.send:
+            assert np.array_equal(ref.send[q], loc.send[q])
+        for q in ref.recv:
+            assert np.array_equal(ref.recv[q], loc.recv[q])
+        for q in ref.send_heart:
+            assert np.array_equal(ref.send_heart[q], loc.send_heart[q])

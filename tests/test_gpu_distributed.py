@@ -46,3 +46,42 @@ def test_distributed_native_backend_nccl_world1():
             assert rel_l2(xu, xv, g[f"sanity_{inner}_u"], g[f"sanity_{inner}_v"]) <= 1e-8
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_time_step_world1_matches_single_gpu():
+    """DistributedSimulation at world size 1 (NCCL) = the single-GPU time step:
+    with one block, block-Jacobi IC(0) is the full IC(0)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1711_08708_b200 as bd
+    from paper_1711_08708_b200 import configs
+    from paper_1711_08708_b200 import distributed as D
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        wl = configs.cfg2((12, 12, 6), steps=5)
+        part = D.rcb_partition(wl.mesh.vertices, 1)
+        sim = D.DistributedSimulation(wl, part, 0, 1, dist, torch.device("cuda", 0))
+        state = sim.resting()
+        sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers)
+        pre = bd.BlockLUPreconditioner(sysm, inner="ic0")
+        ref = bd.SimState.resting(sysm.n, sysm.n_heart, wl.ionic)
+        lp = sim.lp
+        for _ in range(5):
+            state, st = sim.step(state)
+            ref, rst = bd.time_step(ref, sysm, pre, wl.ionic, wl.protocol, wl.dt, tol=wl.tol,
+                                    max_iter=20000)
+            assert abs(st["iterations"] - rst.iterations) <= 1
+            u = np.zeros(lp.n_own)
+            u[lp.owned] = state[0].cpu().numpy()
+            v = np.zeros(lp.m_own)
+            v[lp.owned[: lp.m_own]] = state[1].cpu().numpy()
+            assert rel_l2(u, v, ref.u.cpu().numpy(), ref.v.cpu().numpy()) <= 1e-9
+    finally:
+        dist.destroy_process_group()

@@ -19,7 +19,8 @@ HEADER = os.path.join(REPO, "include", "bidomain_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(bd_[a-z0-9_]+)\s*\(", text)))
+    decl = r"^(?:bd_status|const char\*|int64_t)\s+(bd_[a-z0-9_]+)\s*\("
+    return sorted(set(re.findall(decl, text, flags=re.M)))
 
 
 def test_library_exports_every_header_symbol():
