@@ -262,7 +262,7 @@ def run_native(args, rank, world, local_rank):
     if os.path.exists(ncu_path):
         with open(ncu_path) as fh:
             traffic = json.load(fh).get(
-                f"{wl.name}_{wl.inner}_{os.environ.get('BD_TRSV', 'dtile')}_bulk_solve_bytes")
+                f"{wl.name}_{wl.inner}_{os.environ.get('BD_TRSV', 'btile')}_bulk_solve_bytes")
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -287,7 +287,7 @@ def run_native(args, rank, world, local_rank):
                     "wall_s": round(wall_e2e, 3)},
             "roofline": {"bound": "hbm",
                          "kernel": ("bulk inner solve pair: forward + backward triangular pass "
-                                    f"(k_trsv_{os.environ.get('BD_TRSV', 'dtile')}, P_1 block)")
+                                    f"(k_trsv_{os.environ.get('BD_TRSV', 'btile')}, P_1 block)")
                                    if wl.inner != "jacobi" else "jacobi",
                          "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",

@@ -134,6 +134,22 @@ struct DevDTile {
   }
 };
 
+struct DevBTile {
+  int* tile_nr = nullptr;
+  int* task_row = nullptr;
+  int* ext_slot = nullptr;
+  double* ext_val = nullptr;
+  int* in_col = nullptr;
+  double* inv = nullptr;
+  int ntiles = 0, rs = 0, xs = 0, is = 0, Ex = 4, grid = 0, threads = 256, sleep_ns = 0,
+      prefetch = 1;
+  size_t smem = 0;
+  dev::BTileDev dev() const {
+    return dev::BTileDev{tile_nr, task_row, ext_slot, ext_val, in_col,   inv,     ntiles,
+                         rs,      xs,       is,       sleep_ns, prefetch};
+  }
+};
+
 struct DevSuper {
   int* sn_start = nullptr;
   int* sn_size = nullptr;
@@ -154,6 +170,8 @@ struct bd_inner {
   DevCluster CL, CU;
   bool dtile = false;
   DevDTile DL, DU;
+  bool btile = false;
+  DevBTile BL, BU;
   double* rtmp = nullptr;
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
@@ -736,9 +754,13 @@ bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
                       const double* coords, int dim) {
   bd_ctx* ctx = p->ctx;
   const int target = getenv("BD_DTILE_ROWS") ? atoi(getenv("BD_DTILE_ROWS")) : 64;
-  const int ntiles = (int)std::max<int64_t>(1, lower.n / target);
+  const char* part = getenv("BD_TILE_PART");
+  const bool grid = !(part && std::string(part) == "rcb");
+  int ntiles = (int)std::max<int64_t>(1, lower.n / target);
   std::vector<int32_t> tile;
-  if (coords && dim > 0)
+  if (coords && dim > 0 && grid)
+    ntiles = partition_grid(lower.n, dim, coords, target, nullptr, &tile);
+  else if (coords && dim > 0)
     partition_coords(lower.n, dim, coords, ntiles, &tile);
   else
     partition_rows(lower, ntiles, &tile);
@@ -752,6 +774,12 @@ bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   std::string why;
   bool ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
             build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  if (!ok && coords && dim > 0 && grid) {
+    ntiles = (int)std::max<int64_t>(1, lower.n / target);
+    partition_coords(lower.n, dim, coords, ntiles, &tile);
+    ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
+         build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  }
   if (ok && (std::max(dl.tmax, du.tmax) > dev::DT_MAX_ROWS ||
              std::max(dl.smax, du.smax) > dev::DT_MAX_STEPS)) {
     ok = false;
@@ -765,6 +793,145 @@ bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   TRY(upload_dtile(ctx, du, &p->DU));
   p->G = E;
   p->dtile = true;
+  return BD_OK;
+}
+
+bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
+  // re-lay the schedule out with fixed per-tile strides
+  const int nt = (int)bs.tile_row_ptr.size() - 1;
+  const int ex = bs.Ex, rs = dev::bt_even(bs.tmax), xs = dev::bt_even(bs.xmax);
+  const int64_t is = dev::bt_even(rs * (rs + 1) / 2);
+  std::vector<int32_t> nr(nt), row((size_t)nt * rs, -1), slot((size_t)nt * rs * ex, -1),
+      in((size_t)nt * xs, -1);
+  std::vector<double> val((size_t)nt * rs * ex, 0.0), inv((size_t)nt * is, 0.0);
+  for (int t = 0; t < nt; ++t) {
+    const int r0 = bs.tile_row_ptr[t], n_ = bs.tile_row_ptr[t + 1] - r0;
+    nr[t] = n_;
+    for (int k = 0; k < n_; ++k) {
+      row[(size_t)t * rs + k] = bs.task_row[r0 + k];
+      for (int e = 0; e < ex; ++e) {
+        slot[((size_t)t * rs + k) * ex + e] = bs.ext_col[(size_t)(r0 + k) * ex + e];
+        val[((size_t)t * rs + k) * ex + e] = bs.ext_val[(size_t)(r0 + k) * ex + e];
+      }
+    }
+    const int x0 = bs.tile_in_ptr[t], nx = bs.tile_in_ptr[t + 1] - x0;
+    for (int j = 0; j < nx; ++j) in[(size_t)t * xs + j] = bs.in_col[x0 + j];
+    const int64_t i0 = bs.tile_inv_ptr[t], ni = bs.tile_inv_ptr[t + 1] - i0;
+    std::copy(bs.inv.begin() + i0, bs.inv.begin() + i0 + ni, inv.begin() + (size_t)t * is);
+  }
+  CK(ctx, upload_vec(&out->tile_nr, nr));
+  CK(ctx, upload_vec(&out->task_row, row));
+  CK(ctx, upload_vec(&out->ext_slot, slot));
+  CK(ctx, upload_vec(&out->ext_val, val));
+  CK(ctx, upload_vec(&out->in_col, in));
+  CK(ctx, upload_vec(&out->inv, inv));
+  out->ntiles = nt;
+  out->rs = rs;
+  out->xs = xs;
+  out->is = (int)is;
+  out->Ex = ex;
+  out->threads = std::min(256, std::max(32, dev::BT_LANES * ((bs.tmax + 7) / 8 * 8)));
+  out->threads = std::max(out->threads, std::min(256, (rs + 31) / 32 * 32));
+  if (getenv("BD_BTILE_THREADS"))
+    out->threads = std::max((rs + 31) / 32 * 32,
+                            std::min(256, atoi(getenv("BD_BTILE_THREADS")) / 32 * 32));
+  out->threads = std::max(out->threads, ((xs + 1) / 2 + 31) / 32 * 32);  // <= 2 inputs per thread
+  out->sleep_ns = getenv("BD_BTILE_SLEEP") ? atoi(getenv("BD_BTILE_SLEEP")) : 0;
+  out->prefetch = getenv("BD_BTILE_PREFETCH") ? atoi(getenv("BD_BTILE_PREFETCH")) : 1;
+  out->smem = sizeof(double) * ((size_t)rs + (size_t)xs + (size_t)is);
+  auto k4 = dev::k_trsv_btile<4, dev::RhsGather>;
+  auto k8 = dev::k_trsv_btile<8, dev::RhsGather>;
+  auto kv4 = dev::k_trsv_btile<4, dev::RhsVec>;
+  auto kv8 = dev::k_trsv_btile<8, dev::RhsVec>;
+  auto ks4 = dev::k_trsv_btile<4, dev::RhsSchur>;
+  auto ks8 = dev::k_trsv_btile<8, dev::RhsSchur>;
+  // the attribute is per kernel, shared by every schedule: only ever raise it
+  static size_t smem_attr = 0;
+  if (out->smem > smem_attr) {
+    const int sm = (int)out->smem;
+    for (auto k : {k4, k8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    for (auto k : {kv4, kv8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    for (auto k : {ks4, ks8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    smem_attr = out->smem;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, out->Ex == 4 ? k4 : k8, out->threads,
+                                                out->smem);
+  out->grid = (int)std::min<int64_t>(out->ntiles, (int64_t)ctx->nsm * std::max(1, per_sm));
+  if (getenv("BD_DEBUG"))
+    std::fprintf(stderr, "[bd] btile launch: %d threads, %zu B smem, %d CTAs/SM, grid %d\n",
+                 out->threads, out->smem, per_sm, out->grid);
+  return BD_OK;
+}
+
+void free_btile(DevBTile* d) {
+  cudaFree(d->tile_nr);
+  cudaFree(d->task_row);
+  cudaFree(d->ext_slot);
+  cudaFree(d->ext_val);
+  cudaFree(d->in_col);
+  cudaFree(d->inv);
+}
+
+bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
+                      const double* coords, int dim) {
+  bd_ctx* ctx = p->ctx;
+  const int target = getenv("BD_BTILE_ROWS") ? atoi(getenv("BD_BTILE_ROWS")) : 64;
+  const char* part = getenv("BD_TILE_PART");  // "grid" (default) | "rcb"
+  const bool grid = !(part && std::string(part) == "rcb");
+  int ntiles = (int)std::max<int64_t>(1, lower.n / target);
+  std::vector<int32_t> tile;
+  if (coords && dim > 0 && grid)
+    ntiles = partition_grid(lower.n, dim, coords, target, nullptr, &tile);
+  else if (coords && dim > 0)
+    partition_coords(lower.n, dim, coords, ntiles, &tile);
+  else
+    partition_rows(lower, ntiles, &tile);
+  int E = 4;
+  for (int64_t i = 0; i < lower.n; ++i)
+    while (E < lower.indptr[i + 1] - lower.indptr[i] - 1) E <<= 1;
+  for (int64_t i = 0; i < upper.n; ++i)
+    while (E < upper.indptr[i + 1] - upper.indptr[i] - 1) E <<= 1;
+  DTileSchedule dl, du;
+  BTileSchedule bl, bu;
+  std::string why;
+  bool ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
+            build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  if (!ok && coords && dim > 0 && grid) {  // e.g. a cyclic tile graph: fall back to RCB tiles
+    ntiles = (int)std::max<int64_t>(1, lower.n / target);
+    partition_coords(lower.n, dim, coords, ntiles, &tile);
+    ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
+         build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  }
+  ok = ok && build_btile_schedule(dl, &bl, &why) && build_btile_schedule(du, &bu, &why);
+  if (ok && (std::max(bl.tmax, bu.tmax) > 256 || std::max(bl.Ex, bu.Ex) > 8 ||
+             std::max(bl.xmax, bu.xmax) > 512 ||
+             std::max(bl.tmax, bu.tmax) > (int)std::sqrt(2.0 * 24000))) {
+    ok = false;
+    why = "tile too large or too many external entries";
+  }
+  if (getenv("BD_DEBUG"))
+    std::fprintf(stderr, "[bd] btile n=%lld tiles=%d: %s (tmax %d, Ex %d/%d, inv %.1f MB)\n",
+                 (long long)lower.n, ntiles, ok ? "ok" : why.c_str(), bl.tmax, bl.Ex, bu.Ex,
+                 8e-6 * (double)(bl.inv.size() + bu.inv.size()));
+  if (!ok) return BD_OK;
+  TRY(upload_btile(ctx, bl, &p->BL));
+  TRY(upload_btile(ctx, bu, &p->BU));
+  p->btile = true;
+  return BD_OK;
+}
+
+template <class Rhs>
+bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
+                       int ctr_task, int ctr_done) {
+  bd_ctx* ctx = p->ctx;
+  if (b.Ex == 4)
+    dev::k_trsv_btile<4, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
+                                                                           ctr_task, ctr_done);
+  else
+    dev::k_trsv_btile<8, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
+                                                                           ctr_task, ctr_done);
+  LAUNCHED(ctx);
   return BD_OK;
 }
 
@@ -824,6 +991,17 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->btile) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1));
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3));
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->dtile) {
@@ -1467,17 +1645,20 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   }
   if (st == BD_OK && kind == BD_INNER_IC0) {
     const char* mode = getenv("BD_TRSV");
-    const std::string m = mode ? mode : "dtile";
+    const std::string m = mode ? mode : "btile";
     if (m == "cluster") {
       st = setup_cluster(p, lower, upper, coords, dim);
     }
-    if (m == "dtile") {
+    if (m == "btile") {
+      st = setup_btile(p, lower, upper, coords, dim);
+    }
+    if (m == "dtile" || (m == "btile" && st == BD_OK && !p->btile)) {
       st = setup_dtile(p, lower, upper, coords, dim);
     }
     if (m == "tiled" || m == "rows") {
       p->rows_mode = (m == "rows");
       st = setup_tiles(p, lower, upper, coords, dim);
-    } else if (m == "persist" || (m == "cluster" && !p->cluster) || (m == "dtile" && !p->dtile)) {
+    } else if (m == "persist" || (m == "cluster" && !p->cluster) || ((m == "dtile" || m == "btile") && !p->dtile && !p->btile)) {
       int64_t maxoff = 0;
       for (int64_t i = 0; i < n; ++i)
         maxoff = std::max<int64_t>(maxoff, lower.indptr[i + 1] - lower.indptr[i] - 1);
@@ -1528,6 +1709,8 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_cluster(&p->CU);
   free_dtile(&p->DL);
   free_dtile(&p->DU);
+  free_btile(&p->BL);
+  free_btile(&p->BU);
   cudaFree(p->rtmp);
   cudaFree(p->perm);
   cudaFree(p->inv);
@@ -1551,6 +1734,18 @@ bd_status bd_inner_apply(bd_inner* p, const double* y, double* z) {
 bd_status bd_debug_tile_trace(void* dev_buf, int steps) {
   cudaMemcpyToSymbol(dev::g_tile_trace, &dev_buf, sizeof(void*));
   cudaMemcpyToSymbol(dev::g_tile_trace_steps, &steps, sizeof(int));
+  return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ECUDA;
+}
+
+// Debug: first row of every blocked tile of one pass (0 forward, 1 backward)
+// in task order; returns the tile count in *ntiles.  Not in the public header.
+bd_status bd_debug_btile_rows(bd_inner* p, int pass, int32_t* first_row, int* ntiles) {
+  if (!p || !p->btile) return BD_EINVAL;
+  const DevBTile& b = pass ? p->BU : p->BL;
+  *ntiles = b.ntiles;
+  if (!first_row) return BD_OK;
+  for (int t = 0; t < b.ntiles; ++t)
+    cudaMemcpy(first_row + t, b.task_row + (size_t)t * b.rs, sizeof(int32_t), cudaMemcpyDeviceToHost);
   return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ECUDA;
 }
 

@@ -1410,6 +1410,162 @@ __global__ void __launch_bounds__(256) k_trsv_dtile(DTileDev T, Rhs rhs, double*
   }
 }
 
+// ---- blocked-tile triangular solve ------------------------------------------
+// Same tiles and priority-topological tile order as k_trsv_dtile, but a tile
+// no longer walks its ~10 internal levels: it gathers b_T - L_T,ext x_ext once
+// (one thread per row, polling only the entries that reach other tiles), then
+// applies the precomputed dense inverse of its diagonal block from shared
+// memory (4 lanes per row + shuffles).  The inverse is copied in with cp.async
+// as soon as the tile is grabbed, i.e. while its inputs are still in flight,
+// so a pass costs ~(tile-DAG depth) x (one cross-SM hop + a short dense step).
+struct BTileDev {
+  // fixed per-tile strides: every load of a tile depends on the tile id only
+  const int* tile_nr;    // rows of each tile
+  const int* task_row;   // [tile][RS] (-1 padding)
+  const int* ext_slot;   // [tile][RS][EX]: slot in the tile's input list (-1 padding)
+  const double* ext_val;
+  const int* in_col;     // [tile][XS] (-1 padding)
+  const double* inv;     // [tile][IS] packed lower triangle (slot order)
+  int ntiles;
+  int rs, xs, is;        // strides (rows, inputs, inverse doubles; all even)
+  int sleep_ns;          // cap of the polling back-off (0: spin)
+  int prefetch;          // L2 bulk prefetch of the tile one grid-width ahead
+};
+constexpr int BT_LANES = 4;  // lanes per row in the dense step
+
+__host__ __device__ constexpr int bt_even(int v) { return (v + 1) & ~1; }
+
+template <int EX, class Rhs>
+__global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double* __restrict__ xg,
+                                                    Ctl c, int ctr_task, int ctr_done) {
+  if (inactive(c)) return;
+  extern __shared__ __align__(16) double bt_sm[];
+  double* ys = bt_sm;        // rs
+  double* xin = ys + T.rs;   // xs external inputs
+  double* is = xin + T.xs;   // packed inverse
+  __shared__ int task_s;
+  __shared__ int last_s;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (;;) {
+    if (tid == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+    __syncthreads();
+    const int t = task_s;
+    if (t >= T.ntiles) break;
+    unsigned long long* trace = g_tile_trace;
+    if (trace && tid == 0) trace[6 * t] = gtimer();
+    if (tid == 0 && T.prefetch && t + (int)gridDim.x < T.ntiles) {
+      const int u = t + (int)gridDim.x;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(T.inv + (int64_t)u * T.is),
+                   "r"((unsigned)(T.is * 8)) : "memory");
+    }
+    // everything below up to the polls depends on t only (one round trip)
+    const int nr = T.tile_nr[t];
+    int row = -1;
+    int sl[EX];
+    double vl[EX];
+    const int64_t rb = (int64_t)t * T.rs + tid;
+    if (tid < T.rs) {
+      row = T.task_row[rb];
+#pragma unroll
+      for (int e = 0; e < EX; ++e) {
+        sl[e] = T.ext_slot[rb * EX + e];
+        vl[e] = T.ext_val[rb * EX + e];
+      }
+    }
+    int icol[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * nth;
+      icol[h] = j < T.xs ? T.in_col[(int64_t)t * T.xs + j] : -1;
+    }
+    // inverse block -> smem (independent of x); size from the tile's row count
+    const int ninv = bt_even(nr * (nr + 1) / 2);
+    const double* ib = T.inv + (int64_t)t * T.is;
+    for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is + 2 * q, ib + 2 * q);
+    cp_async_commit();
+    const double b = rhs.template eval<1>(row, 0);
+    if (trace) {
+      __syncthreads();
+      if (tid == 0) trace[6 * t + 5] = gtimer();
+    }
+    // the tile's distinct inputs: one poller each
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (icol[h] < 0) continue;
+      const double* pj = &xg[icol[h]];
+      long long v;
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+      unsigned nap = 16;
+      while (v == SENTINEL) {
+        if (T.sleep_ns) {
+          __nanosleep(nap);
+          nap = min(2u * nap, (unsigned)T.sleep_ns);
+        }
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+      }
+      xin[tid + h * nth] = __longlong_as_double(v);
+    }
+    __syncthreads();
+    if (trace && tid == 0) trace[6 * t + 4] = gtimer();
+    if (row >= 0) {
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < EX; ++e) acc = fma(vl[e], sl[e] >= 0 ? xin[sl[e] < 0 ? 0 : sl[e]] : 0.0, acc);
+      ys[tid] = __dsub_rn(b, acc);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (trace && tid == 0) trace[6 * t + 1] = gtimer();
+    // x_k = sum_{l<=k} inv[k][l] y_l
+    const int q = tid & (BT_LANES - 1);
+    for (int base = 0; base < nr; base += nth / BT_LANES) {
+      const int k = base + tid / BT_LANES;
+      double s = 0.0;
+      if (k < nr) {
+        // 16 entries per lane per round: all shared loads issued before the FMAs
+        const double* ik = is + (k * (k + 1) >> 1);
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l0 = q; l0 <= k; l0 += 4 * 4 * BT_LANES) {
+          double a[16], yv[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int l = l0 + u * BT_LANES;
+            a[u] = l <= k ? ik[l] : 0.0;
+            yv[u] = l <= k ? ys[l] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) s4[u & 3] = fma(a[u], yv[u], s4[u & 3]);
+        }
+        s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      }
+#pragma unroll
+      for (int o = 1; o < BT_LANES; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (q == 0 && k < nr) {
+        const int rk = (k == tid) ? row : T.task_row[(int64_t)t * T.rs + k];
+        publish(&xg[rk], s);
+      }
+    }
+    __syncthreads();  // smem reuse by the next tile
+    if (trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[6 * t + 2] = gtimer();
+      trace[6 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && tid == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
+}
+
 // ---- persistent sync-free triangular solve ----------------------------------
 // Tasks (rows) in level order, ELL entries (G per row, column -1 = padding)
 // stored in task order so a chunk of rows is one contiguous, coalesced read.

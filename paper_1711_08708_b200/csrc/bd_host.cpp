@@ -889,4 +889,135 @@ bool build_dtile_schedule(const HostCsr& t, bool lower, const std::vector<int32_
   return true;
 }
 
+bool build_btile_schedule(const DTileSchedule& ds, BTileSchedule* out, std::string* why) {
+  const int E = ds.E;
+  const int ntiles = (int)ds.tile_row_ptr.size() - 1;
+  const int64_t nt = (int64_t)ds.task_row.size();
+  const int32_t zero = -(ds.tmax + 1);
+  int ex = 1;
+  for (int64_t k = 0; k < nt; ++k) {
+    int c = 0;
+    for (int e = 0; e < E; ++e) c += ds.ell_col[k * E + e] >= 0;
+    ex = std::max(ex, c);
+  }
+  ex = ex <= 4 ? 4 : ex <= 8 ? 8 : ex;  // device kernels are instantiated for widths 4 and 8
+  out->Ex = ex;
+  out->tmax = ds.tmax;
+  out->tile_row_ptr = ds.tile_row_ptr;
+  out->task_row = ds.task_row;
+  out->ext_col.assign(nt * ex, -1);
+  out->ext_val.assign(nt * ex, 0.0);
+  out->tile_inv_ptr.assign(1, 0);
+  out->inv.clear();
+  out->tile_in_ptr.assign(1, 0);
+  out->in_col.clear();
+  out->xmax = 0;
+  std::vector<int32_t> loc;
+  for (int t = 0; t < ntiles; ++t) {
+    const int r0 = ds.tile_row_ptr[t], r1 = ds.tile_row_ptr[t + 1];
+    loc.clear();
+    for (int64_t k = r0; k < r1; ++k)
+      for (int e = 0; e < E; ++e)
+        if (ds.ell_col[k * E + e] >= 0) loc.push_back(ds.ell_col[k * E + e]);
+    std::sort(loc.begin(), loc.end());
+    loc.erase(std::unique(loc.begin(), loc.end()), loc.end());
+    for (int64_t k = r0; k < r1; ++k) {
+      int c = 0;
+      for (int e = 0; e < E; ++e) {
+        const int32_t code = ds.ell_col[k * E + e];
+        if (code >= 0) {
+          out->ext_col[k * ex + c] = (int32_t)(std::lower_bound(loc.begin(), loc.end(), code) - loc.begin());
+          out->ext_val[k * ex + c] = ds.ell_val[k * E + e];
+          ++c;
+        }
+      }
+    }
+    out->in_col.insert(out->in_col.end(), loc.begin(), loc.end());
+    out->tile_in_ptr.push_back((int32_t)out->in_col.size());
+    out->xmax = std::max<int>(out->xmax, (int)loc.size());
+  }
+  std::vector<long double> x;
+  for (int t = 0; t < ntiles; ++t) {
+    const int r0 = ds.tile_row_ptr[t], nr = ds.tile_row_ptr[t + 1] - r0;
+    // X = A^{-1} for the tile block A (lower triangular in slot order):
+    // X[k][l] = (delta_kl - sum_{l<=j<k} A[k][j] X[j][l]) / A[k][k]
+    x.assign((size_t)nr * nr, 0.0L);
+    for (int k = 0; k < nr; ++k) {
+      const int64_t q = r0 + k;
+      const long double d = ds.task_diag[q];
+      if (!(d != 0.0L)) {
+        *why = "zero pivot in a tile block";
+        return false;
+      }
+      for (int e = 0; e < E; ++e) {
+        const int32_t code = ds.ell_col[q * E + e];
+        if (code >= 0 || code == zero) continue;
+        const int j = -code - 1;
+        if (j >= k) {
+          *why = "tile block is not triangular in slot order";
+          return false;
+        }
+        const long double a = ds.ell_val[q * E + e];
+        for (int l = 0; l <= j; ++l) x[(size_t)k * nr + l] -= a * x[(size_t)j * nr + l];
+      }
+      x[(size_t)k * nr + k] += 1.0L;
+      for (int l = 0; l <= k; ++l) x[(size_t)k * nr + l] /= d;
+    }
+    for (int k = 0; k < nr; ++k)
+      for (int l = 0; l <= k; ++l) out->inv.push_back((double)x[(size_t)k * nr + l]);
+    if (out->inv.size() & 1) out->inv.push_back(0.0);
+    out->tile_inv_ptr.push_back((int64_t)out->inv.size());
+  }
+  return true;
+}
+
+int partition_grid(int64_t n, int dim, const double* coords, int target,
+                   const std::vector<int32_t>* cls, std::vector<int32_t>* tile) {
+  const int k = std::max(1, (int)std::lround(std::pow((double)target, 1.0 / dim)));
+  std::vector<int64_t> bin(n, 0);
+  int64_t stride = 1;
+  for (int a = 0; a < dim; ++a) {
+    std::vector<double> v(n);
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+      v[i] = coords[i * dim + a];
+      lo = std::min(lo, v[i]);
+      hi = std::max(hi, v[i]);
+    }
+    const double tol = 1e-9 * std::max(1.0, hi - lo);
+    std::vector<double> u(v);
+    std::sort(u.begin(), u.end());
+    std::vector<double> uniq;
+    for (double x : u)
+      if (uniq.empty() || x - uniq.back() > tol) uniq.push_back(x);
+    const double limit = 8.0 * std::pow((double)n, 1.0 / dim);
+    int64_t nb;
+    std::vector<int64_t> b(n);
+    if ((double)uniq.size() <= limit) {  // structured axis: bin by layer rank
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = std::lower_bound(uniq.begin(), uniq.end(), v[i] - tol) - uniq.begin();
+        b[i] = r / k;
+      }
+      nb = ((int64_t)uniq.size() + k - 1) / k;
+    } else {  // unstructured: equal-width bins holding ~k layers of points
+      nb = std::max<int64_t>(1, (int64_t)std::llround(std::pow((double)n, 1.0 / dim) / k));
+      const double w = (hi - lo) / (double)nb;
+      for (int64_t i = 0; i < n; ++i)
+        b[i] = std::min<int64_t>(nb - 1, w > 0 ? (int64_t)((v[i] - lo) / w) : 0);
+    }
+    for (int64_t i = 0; i < n; ++i) bin[i] += b[i] * stride;
+    stride *= nb;
+  }
+  if (cls)
+    for (int64_t i = 0; i < n; ++i) bin[i] += stride * (int64_t)(*cls)[i];
+  // compact to dense tile ids
+  std::vector<int64_t> keys(bin);
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  tile->resize(n);
+  for (int64_t i = 0; i < n; ++i)
+    (*tile)[i] = (int32_t)(std::lower_bound(keys.begin(), keys.end(), bin[i]) - keys.begin());
+  return (int)keys.size();
+}
+
 }  // namespace bd

@@ -60,6 +60,14 @@ void partition_rows(const HostCsr& a, int parts, std::vector<int32_t>* part);
 // quantile).  On structured meshes numbered lexicographically the lower-
 // triangular dependencies point to smaller coordinates, so the part DAG of a
 // triangular solve is acyclic with chains of length ~ the box grid diameter.
+// Lattice-aligned tiles: bin every axis into slabs of ~k = target^(1/dim)
+// coordinate layers (by the rank of the distinct coordinate value when the
+// axis has few distinct values, i.e. a structured grid; by equal-width bins
+// otherwise) and split by `cls` (e.g. heart / torso) so that the tile DAG of a
+// natural ordering stays acyclic and its depth is ~sum of bins per axis.
+// Returns the number of (non-empty) tiles.
+int partition_grid(int64_t n, int dim, const double* coords, int target,
+                   const std::vector<int32_t>* cls, std::vector<int32_t>* tile);
 void partition_coords(int64_t n, int dim, const double* coords, int parts,
                       std::vector<int32_t>* part);
 
@@ -139,5 +147,23 @@ struct DTileSchedule {
 };
 bool build_dtile_schedule(const HostCsr& t, bool lower, const std::vector<int32_t>& tile,
                           int ntiles, int E, DTileSchedule* out, std::string* why);
+
+// Blocked-tile schedule derived from a DTileSchedule (same tiles, same task
+// order): per tile the dense inverse of its diagonal block (lower triangular
+// in slot order, packed row-major, each block padded to an even length so it
+// is 16-byte aligned) and per row only the entries that reach other tiles.
+// A pass is then y_T = b_T - L_T,ext x_ext ; x_T = inv(L_TT) y_T.
+struct BTileSchedule {
+  int Ex = 0, tmax = 0, xmax = 0;
+  std::vector<int32_t> tile_row_ptr;  // ntiles+1 (task order)
+  std::vector<int64_t> tile_inv_ptr;  // ntiles+1 (doubles)
+  std::vector<int32_t> task_row;
+  std::vector<int32_t> ext_col;       // ntasks*Ex: slot in the tile's input list, -1 = padding
+  std::vector<double> ext_val;
+  std::vector<int32_t> tile_in_ptr;   // ntiles+1: distinct external inputs of each tile
+  std::vector<int32_t> in_col;        // their global rows
+  std::vector<double> inv;
+};
+bool build_btile_schedule(const DTileSchedule& ds, BTileSchedule* out, std::string* why);
 
 }  // namespace bd

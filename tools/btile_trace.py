@@ -1,0 +1,79 @@
+"""Dev tool: per-tile timestamps of the blocked-tile triangular solve on cfg2
+(grab, inputs ready, published) for the backward pass of one IC(0) apply, and
+the critical path split into hop (ready - last dependency published) and
+compute (published - ready).  Tiles are lattice bins, deps = the +1 bins."""
+import ctypes as C, os, sys
+import numpy as np
+sys.path.insert(0, '/root/repo')
+os.environ.setdefault("BD_TRSV", "btile")
+import torch
+import paper_1711_08708_b200 as bd
+from paper_1711_08708_b200 import configs, _lib
+from paper_1711_08708_b200.assembly import assemble_stiffness
+from paper_1711_08708_b200.conductivity import TensorField
+from paper_1711_08708_b200.precond import regularize_stiffness
+cells = tuple(int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "128,128,64").split(","))
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+wl = configs.cfg2(cells)
+S1 = assemble_stiffness(wl.mesh, TensorField(wl.params, 3, "bar1", wl.fibers))
+g = regularize_stiffness(S1).grounded()
+inner = bd.IncompleteCholesky0(); inner.setup(g, coords=wl.mesh.vertices)
+L = _lib.lib()
+L.bd_debug_tile_trace.argtypes = [C.c_void_p, C.c_int]
+L.bd_debug_btile_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+ntc = C.c_int()
+L.bd_debug_btile_rows(inner.handle, 1, None, C.byref(ntc)); nt = ntc.value
+first = np.zeros(nt, dtype=np.int32)
+L.bd_debug_btile_rows(inner.handle, 1, first.ctypes.data, C.byref(ntc))
+V = wl.mesh.vertices
+rank = [np.searchsorted(np.unique(V[:, a]), V[first, a]) for a in range(3)]
+bins = np.stack([r // 4 for r in rank], 1)
+key = {tuple(b): t for t, b in enumerate(bins)}
+buf = torch.zeros(nt * 6 + 8, dtype=torch.int64, device='cuda')
+y = torch.as_tensor(np.random.default_rng(0).standard_normal(g.shape[0])).cuda()
+for _ in range(3):
+    inner.apply_inverse(y)
+torch.cuda.synchronize()
+for rep in range(reps):
+    buf.zero_()
+    L.bd_debug_tile_trace(C.c_void_p(buf.data_ptr()), 1)
+    inner.apply_inverse(y); torch.cuda.synchronize()
+    L.bd_debug_tile_trace(None, 0)
+    tr = buf[: nt * 6].view(nt, 6).cpu().numpy().astype(np.int64)
+    t0 = tr[:, 0].min()
+    grab, ready, done = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
+    polled, prep = (tr[:, 4] - t0) / 1e3, (tr[:, 5] - t0) / 1e3
+    deps = []
+    for t in range(nt):
+        b = bins[t]
+        d = [key[(b[0] + a, b[1] + c, b[2] + e)] for a in (0, 1) for c in (0, 1) for e in (0, 1)
+             if (a, c, e) != (0, 0, 0) and (b[0] + a, b[1] + c, b[2] + e) in key]
+        deps.append(d)
+    last_dep = np.array([max(done[d]) if d else 0.0 for d in deps])
+    hop = ready - np.maximum(last_dep, grab)
+    comp = done - ready
+    # critical path from the last-finishing tile
+    t = int(np.argmax(done)); path = []
+    while True:
+        path.append(t)
+        if not deps[t]:
+            break
+        t = max(deps[t], key=lambda q: done[q])
+    path = path[::-1]
+    ph, pc = hop[path], comp[path]
+    pre = np.array([max(0.0, grab[q] - (max(done[deps[q]]) if deps[q] else 0)) for q in path])
+    print(f"rep {rep}: span {done.max():.1f} us, critical path {len(path)} tiles: "
+          f"hop sum {ph.sum():.1f} (median {np.median(ph):.2f}), compute sum {pc.sum():.1f} "
+          f"(median {np.median(pc):.2f}), grab-after-ready sum {pre.sum():.1f}")
+    print("   all tiles: hop median %.2f p90 %.2f; compute median %.2f p90 %.2f" % (
+        np.median(hop), np.percentile(hop, 90), np.median(comp), np.percentile(comp, 90)))
+    p_poll = polled[path] - np.maximum(last_dep[path], prep[path])
+    p_cp = ready[path] - polled[path]
+    p_prep = prep[path] - grab[path]
+    print(f"   path: poll-after-max(dep,prep) sum {p_poll.sum():.1f} median {np.median(p_poll):.2f}; "
+          f"polled->ready sum {p_cp.sum():.1f} median {np.median(p_cp):.2f}; grab->prep median {np.median(p_prep):.2f}; "
+          f"prep after last dep: {(prep[path] > last_dep[path]).sum()} tiles")
+    seg = np.array_split(np.arange(len(path)), 6)
+    print("   path poll/cp by segment:", [(round(p_poll[s_].mean(), 2), round(p_cp[s_].mean(), 2)) for s_ in seg])
+    print("   path hop/compute by segment:", [(round(ph[s].mean(), 2), round(pc[s].mean(), 2)) for s in seg])
+np.save("/root/repo/gpurun_out/btile_trace.npy", tr)

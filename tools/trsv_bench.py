@@ -25,15 +25,18 @@ for mode in os.environ.get("MODES", "persist,tiled,syncfree").split(","):
     inner = bd.IncompleteCholesky0(); t0 = time.time(); inner.setup(g, coords=wl.mesh.vertices)
     print(mode, "setup", round(time.time()-t0, 2), "s", inner.factor_info(), flush=True)
     z = inner.apply_inverse(y); torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record()
+    for k in range(reps):
         z = inner.apply_inverse(y)
-    e1.record(); torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+        ev[k + 1].record()
+    torch.cuda.synchronize()
+    per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(reps)])
+    ms = float(np.median(per))
+    print(f"{mode}: per-rep us min {per.min()*1e3:.1f} median {ms*1e3:.1f} max {per.max()*1e3:.1f}")
     nnz = inner.factor_info()["nnz"]; n = g.shape[0]
     byts = 2 * (12 * nnz + 4 * (n + 1) + 16 * n)
-    print(f"{mode}: {ms*1e3:.1f} us per apply (fwd+bwd) -> {byts/ms/1e6:.0f} GB/s algorithmic", flush=True)
+    print(f"{mode}: {ms*1e3:.1f} us per apply (median, fwd+bwd) -> {byts/ms/1e6:.0f} GB/s algorithmic", flush=True)
     res[mode] = z.cpu().numpy()
 ks = list(res)
 for k in ks[1:]:
