@@ -137,16 +137,18 @@ struct DevDTile {
 struct DevBTile {
   int* tile_nr = nullptr;
   int* task_row = nullptr;
-  int* ext_slot = nullptr;
-  double* ext_val = nullptr;
+  unsigned short* ent_rp = nullptr;
+  unsigned short* ent_slot = nullptr;
+  double* ent_val = nullptr;
   int* in_col = nullptr;
   double* inv = nullptr;
-  int ntiles = 0, rs = 0, xs = 0, is = 0, Ex = 4, grid = 0, threads = 256, sleep_ns = 0,
+  int ntiles = 0, rs = 0, xs = 0, is = 0, es = 0, rps = 0, grid = 0, threads = 256, sleep_ns = 0,
       prefetch = 1;
   size_t smem = 0;
   dev::BTileDev dev() const {
-    return dev::BTileDev{tile_nr, task_row, ext_slot, ext_val, in_col,   inv,     ntiles,
-                         rs,      xs,       is,       sleep_ns, prefetch};
+    return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
+                         ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
+                         prefetch};
   }
 };
 
@@ -797,21 +799,38 @@ bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
 }
 
 bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
-  // re-lay the schedule out with fixed per-tile strides
+  // re-lay the schedule out with fixed per-tile strides; external entries as
+  // a compact per-tile list (row ranges, input slots, values)
   const int nt = (int)bs.tile_row_ptr.size() - 1;
   const int ex = bs.Ex, rs = dev::bt_even(bs.tmax), xs = dev::bt_even(bs.xmax);
   const int64_t is = dev::bt_even(rs * (rs + 1) / 2);
-  std::vector<int32_t> nr(nt), row((size_t)nt * rs, -1), slot((size_t)nt * rs * ex, -1),
-      in((size_t)nt * xs, -1);
-  std::vector<double> val((size_t)nt * rs * ex, 0.0), inv((size_t)nt * is, 0.0);
+  const int rps = dev::bt_round8(rs + 1);
+  int emax = 0;
+  for (int t = 0; t < nt; ++t) {
+    int cnt = 0;
+    for (int64_t k = bs.tile_row_ptr[t]; k < bs.tile_row_ptr[t + 1]; ++k)
+      for (int e = 0; e < ex; ++e) cnt += bs.ext_col[k * ex + e] >= 0;
+    emax = std::max(emax, cnt);
+  }
+  const int es = dev::bt_round8(std::max(emax, 1));
+  if (emax > 65535 || bs.xmax > 65535) return fail(ctx, BD_EINVAL, "btile: tile too large");
+  std::vector<int32_t> nr(nt), row((size_t)nt * rs, -1), in((size_t)nt * xs, -1);
+  std::vector<uint16_t> rp((size_t)nt * rps, 0), slot((size_t)nt * es, 0);
+  std::vector<double> val((size_t)nt * es, 0.0), inv((size_t)nt * is, 0.0);
   for (int t = 0; t < nt; ++t) {
     const int r0 = bs.tile_row_ptr[t], n_ = bs.tile_row_ptr[t + 1] - r0;
     nr[t] = n_;
-    for (int k = 0; k < n_; ++k) {
+    int cnt = 0;
+    for (int k = 0; k < rs + 1 && k < rps; ++k) {
+      rp[(size_t)t * rps + k] = (uint16_t)cnt;
+      if (k >= n_) continue;
       row[(size_t)t * rs + k] = bs.task_row[r0 + k];
       for (int e = 0; e < ex; ++e) {
-        slot[((size_t)t * rs + k) * ex + e] = bs.ext_col[(size_t)(r0 + k) * ex + e];
-        val[((size_t)t * rs + k) * ex + e] = bs.ext_val[(size_t)(r0 + k) * ex + e];
+        const int32_t sl = bs.ext_col[(size_t)(r0 + k) * ex + e];
+        if (sl < 0) continue;
+        slot[(size_t)t * es + cnt] = (uint16_t)sl;
+        val[(size_t)t * es + cnt] = bs.ext_val[(size_t)(r0 + k) * ex + e];
+        ++cnt;
       }
     }
     const int x0 = bs.tile_in_ptr[t], nx = bs.tile_in_ptr[t + 1] - x0;
@@ -821,15 +840,17 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   }
   CK(ctx, upload_vec(&out->tile_nr, nr));
   CK(ctx, upload_vec(&out->task_row, row));
-  CK(ctx, upload_vec(&out->ext_slot, slot));
-  CK(ctx, upload_vec(&out->ext_val, val));
+  CK(ctx, upload_vec(&out->ent_rp, rp));
+  CK(ctx, upload_vec(&out->ent_slot, slot));
+  CK(ctx, upload_vec(&out->ent_val, val));
   CK(ctx, upload_vec(&out->in_col, in));
   CK(ctx, upload_vec(&out->inv, inv));
   out->ntiles = nt;
   out->rs = rs;
   out->xs = xs;
   out->is = (int)is;
-  out->Ex = ex;
+  out->es = es;
+  out->rps = rps;
   out->threads = std::min(256, std::max(32, dev::BT_LANES * ((bs.tmax + 7) / 8 * 8)));
   out->threads = std::max(out->threads, std::min(256, (rs + 31) / 32 * 32));
   if (getenv("BD_BTILE_THREADS"))
@@ -838,37 +859,35 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   out->threads = std::max(out->threads, ((xs + 1) / 2 + 31) / 32 * 32);  // <= 2 inputs per thread
   out->sleep_ns = getenv("BD_BTILE_SLEEP") ? atoi(getenv("BD_BTILE_SLEEP")) : 0;
   out->prefetch = getenv("BD_BTILE_PREFETCH") ? atoi(getenv("BD_BTILE_PREFETCH")) : 1;
-  out->smem = sizeof(double) * ((size_t)rs + (size_t)xs + (size_t)is);
-  auto k4 = dev::k_trsv_btile<4, dev::RhsGather>;
-  auto k8 = dev::k_trsv_btile<8, dev::RhsGather>;
-  auto kv4 = dev::k_trsv_btile<4, dev::RhsVec>;
-  auto kv8 = dev::k_trsv_btile<8, dev::RhsVec>;
-  auto ks4 = dev::k_trsv_btile<4, dev::RhsSchur>;
-  auto ks8 = dev::k_trsv_btile<8, dev::RhsSchur>;
+  out->smem = dev::bt_smem(rs, xs, (int)is, es, rps);
+  auto kg = dev::k_trsv_btile<dev::RhsGather>;
+  auto kv = dev::k_trsv_btile<dev::RhsVec>;
+  auto ks = dev::k_trsv_btile<dev::RhsSchur>;
   // the attribute is per kernel, shared by every schedule: only ever raise it
   static size_t smem_attr = 0;
   if (out->smem > smem_attr) {
     const int sm = (int)out->smem;
-    for (auto k : {k4, k8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    for (auto k : {kv4, kv8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    for (auto k : {ks4, ks8}) CK(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(ctx, cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(ctx, cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(ctx, cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     smem_attr = out->smem;
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, out->Ex == 4 ? k4 : k8, out->threads,
-                                                out->smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, out->threads, out->smem);
+  if (getenv("BD_BTILE_PERSM")) per_sm = std::max(1, std::min(per_sm, atoi(getenv("BD_BTILE_PERSM"))));
   out->grid = (int)std::min<int64_t>(out->ntiles, (int64_t)ctx->nsm * std::max(1, per_sm));
   if (getenv("BD_DEBUG"))
-    std::fprintf(stderr, "[bd] btile launch: %d threads, %zu B smem, %d CTAs/SM, grid %d\n",
-                 out->threads, out->smem, per_sm, out->grid);
+    std::fprintf(stderr, "[bd] btile launch: %d threads, %zu B smem, %d CTAs/SM, grid %d, "
+                 "entries/tile max %d\n", out->threads, out->smem, per_sm, out->grid, emax);
   return BD_OK;
 }
 
 void free_btile(DevBTile* d) {
   cudaFree(d->tile_nr);
   cudaFree(d->task_row);
-  cudaFree(d->ext_slot);
-  cudaFree(d->ext_val);
+  cudaFree(d->ent_rp);
+  cudaFree(d->ent_slot);
+  cudaFree(d->ent_val);
   cudaFree(d->in_col);
   cudaFree(d->inv);
 }
@@ -925,12 +944,8 @@ template <class Rhs>
 bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr_task, int ctr_done) {
   bd_ctx* ctx = p->ctx;
-  if (b.Ex == 4)
-    dev::k_trsv_btile<4, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
-                                                                           ctr_task, ctr_done);
-  else
-    dev::k_trsv_btile<8, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
-                                                                           ctr_task, ctr_done);
+  dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+                                                                     ctr_done);
   LAUNCHED(ctx);
   return BD_OK;
 }
@@ -1711,6 +1726,7 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_dtile(&p->DU);
   free_btile(&p->BL);
   free_btile(&p->BU);
+
   cudaFree(p->rtmp);
   cudaFree(p->perm);
   cudaFree(p->inv);

@@ -1420,29 +1420,38 @@ __global__ void __launch_bounds__(256) k_trsv_dtile(DTileDev T, Rhs rhs, double*
 // so a pass costs ~(tile-DAG depth) x (one cross-SM hop + a short dense step).
 struct BTileDev {
   // fixed per-tile strides: every load of a tile depends on the tile id only
-  const int* tile_nr;    // rows of each tile
-  const int* task_row;   // [tile][RS] (-1 padding)
-  const int* ext_slot;   // [tile][RS][EX]: slot in the tile's input list (-1 padding)
-  const double* ext_val;
-  const int* in_col;     // [tile][XS] (-1 padding)
-  const double* inv;     // [tile][IS] packed lower triangle (slot order)
+  const int* tile_nr;               // rows of each tile
+  const int* task_row;              // [tile][rs] (-1 padding)
+  const unsigned short* ent_rp;     // [tile][rps]: per-row ranges into the tile's external entries
+  const unsigned short* ent_slot;   // [tile][es]: slot in the tile's input list
+  const double* ent_val;            // [tile][es]
+  const int* in_col;                // [tile][xs] (-1 padding)
+  const double* inv;                // [tile][is] packed lower triangle (slot order)
   int ntiles;
-  int rs, xs, is;        // strides (rows, inputs, inverse doubles; all even)
-  int sleep_ns;          // cap of the polling back-off (0: spin)
-  int prefetch;          // L2 bulk prefetch of the tile one grid-width ahead
+  int rs, xs, is, es, rps;          // strides (doubles / elements); 16-byte multiples
+  int sleep_ns;                     // cap of the polling back-off (0: spin)
+  int prefetch;                     // L2 bulk prefetch of the tile one grid-width ahead
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
 __host__ __device__ constexpr int bt_even(int v) { return (v + 1) & ~1; }
+__host__ __device__ constexpr int bt_round8(int v) { return (v + 7) & ~7; }
+// shared-memory layout (bytes) of one tile: ys | xin | inv | ent_val | ent_slot | ent_rp
+__host__ __device__ constexpr size_t bt_smem(int rs, int xs, int is, int es, int rps) {
+  return sizeof(double) * ((size_t)rs + xs + is + es) + sizeof(unsigned short) * ((size_t)es + rps);
+}
 
-template <int EX, class Rhs>
+template <class Rhs>
 __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double* __restrict__ xg,
                                                     Ctl c, int ctr_task, int ctr_done) {
   if (inactive(c)) return;
   extern __shared__ __align__(16) double bt_sm[];
-  double* ys = bt_sm;        // rs
-  double* xin = ys + T.rs;   // xs external inputs
-  double* is = xin + T.xs;   // packed inverse
+  double* ys = bt_sm;         // rs
+  double* xin = ys + T.rs;    // xs external inputs
+  double* is = xin + T.xs;    // packed inverse
+  double* ev = is + T.is;     // external entries
+  unsigned short* esl = reinterpret_cast<unsigned short*>(ev + T.es);
+  unsigned short* erp = esl + T.es;
   __shared__ int task_s;
   __shared__ int last_s;
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -1460,29 +1469,26 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
     }
     // everything below up to the polls depends on t only (one round trip)
     const int nr = T.tile_nr[t];
-    int row = -1;
-    int sl[EX];
-    double vl[EX];
-    const int64_t rb = (int64_t)t * T.rs + tid;
-    if (tid < T.rs) {
-      row = T.task_row[rb];
-#pragma unroll
-      for (int e = 0; e < EX; ++e) {
-        sl[e] = T.ext_slot[rb * EX + e];
-        vl[e] = T.ext_val[rb * EX + e];
-      }
-    }
+    const int row = tid < T.rs ? T.task_row[(int64_t)t * T.rs + tid] : -1;
     int icol[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = tid + h * nth;
       icol[h] = j < T.xs ? T.in_col[(int64_t)t * T.xs + j] : -1;
     }
-    // inverse block -> smem (independent of x); size from the tile's row count
-    const int ninv = bt_even(nr * (nr + 1) / 2);
-    const double* ib = T.inv + (int64_t)t * T.is;
-    for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is + 2 * q, ib + 2 * q);
-    cp_async_commit();
+    // inverse block and external entries -> smem (independent of x)
+    {
+      const int ninv = bt_even(nr * (nr + 1) / 2);
+      const double* ib = T.inv + (int64_t)t * T.is;
+      for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is + 2 * q, ib + 2 * q);
+      const double* vb = T.ent_val + (int64_t)t * T.es;
+      for (int q = tid; 2 * q < T.es; q += nth) cp_async16(ev + 2 * q, vb + 2 * q);
+      const unsigned short* sb = T.ent_slot + (int64_t)t * T.es;
+      for (int q = tid; 8 * q < T.es; q += nth) cp_async16(esl + 8 * q, sb + 8 * q);
+      const unsigned short* rb = T.ent_rp + (int64_t)t * T.rps;
+      for (int q = tid; 8 * q < T.rps; q += nth) cp_async16(erp + 8 * q, rb + 8 * q);
+      cp_async_commit();
+    }
     const double b = rhs.template eval<1>(row, 0);
     if (trace) {
       __syncthreads();
@@ -1505,15 +1511,15 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
       }
       xin[tid + h * nth] = __longlong_as_double(v);
     }
+    cp_async_wait<0>();
     __syncthreads();
     if (trace && tid == 0) trace[6 * t + 4] = gtimer();
     if (row >= 0) {
       double acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < EX; ++e) acc = fma(vl[e], sl[e] >= 0 ? xin[sl[e] < 0 ? 0 : sl[e]] : 0.0, acc);
+      const int e1 = erp[tid + 1];
+      for (int e = erp[tid]; e < e1; ++e) acc = fma(ev[e], xin[esl[e]], acc);
       ys[tid] = __dsub_rn(b, acc);
     }
-    cp_async_wait<0>();
     __syncthreads();
     if (trace && tid == 0) trace[6 * t + 1] = gtimer();
     // x_k = sum_{l<=k} inv[k][l] y_l
@@ -1525,7 +1531,7 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
         // 16 entries per lane per round: all shared loads issued before the FMAs
         const double* ik = is + (k * (k + 1) >> 1);
         double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int l0 = q; l0 <= k; l0 += 4 * 4 * BT_LANES) {
+        for (int l0 = q; l0 <= k; l0 += 16 * BT_LANES) {
           double a[16], yv[16];
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
@@ -1540,10 +1546,7 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
       }
 #pragma unroll
       for (int o = 1; o < BT_LANES; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (q == 0 && k < nr) {
-        const int rk = (k == tid) ? row : T.task_row[(int64_t)t * T.rs + k];
-        publish(&xg[rk], s);
-      }
+      if (q == 0 && k < nr) publish(&xg[T.task_row[(int64_t)t * T.rs + k]], s);
     }
     __syncthreads();  // smem reuse by the next tile
     if (trace && tid == 0) {

@@ -34,6 +34,8 @@ for mode in os.environ.get("MODES", "persist,tiled,syncfree").split(","):
     per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(reps)])
     ms = float(np.median(per))
     print(f"{mode}: per-rep us min {per.min()*1e3:.1f} median {ms*1e3:.1f} max {per.max()*1e3:.1f}")
+    slow = np.nonzero(per > 1.5 * ms)[0]
+    print(f"{mode}: slow reps (>1.5x median): {slow.tolist()} -> {(per[slow]*1e3).round(0).tolist()}")
     nnz = inner.factor_info()["nnz"]; n = g.shape[0]
     byts = 2 * (12 * nnz + 4 * (n + 1) + 16 * n)
     print(f"{mode}: {ms*1e3:.1f} us per apply (median, fwd+bwd) -> {byts/ms/1e6:.0f} GB/s algorithmic", flush=True)
