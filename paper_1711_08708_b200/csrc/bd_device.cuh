@@ -1443,7 +1443,8 @@ __host__ __device__ constexpr size_t bt_smem(int rs, int xs, int is, int es, int
 
 template <class Rhs>
 __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double* __restrict__ xg,
-                                                    Ctl c, int ctr_task, int ctr_done) {
+                                                    Ctl c, int ctr_task, int ctr_done,
+                                                    double* __restrict__ reset) {
   if (inactive(c)) return;
   extern __shared__ __align__(16) double bt_sm[];
   double* ys = bt_sm;         // rs
@@ -1489,7 +1490,22 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
       for (int q = tid; 8 * q < T.rps; q += nth) cp_async16(erp + 8 * q, rb + 8 * q);
       cp_async_commit();
     }
-    const double b = rhs.template eval<1>(row, 0);
+    double b;
+    if constexpr (Rhs::kScalar) {
+      b = rhs.template eval<1>(row, 0);
+    } else {
+      // gather-heavy right-hand side (e.g. the fused S_i product of the Schur
+      // solve): BT_LANES lanes per row, staged through ys
+      for (int k0 = 0; k0 < T.rs; k0 += nth / BT_LANES) {
+        const int k = k0 + tid / BT_LANES;
+        const int rk = k < T.rs ? T.task_row[(int64_t)t * T.rs + k] : -1;
+        const double v = rhs.template eval<BT_LANES>(rk, tid & (BT_LANES - 1));
+        if ((tid & (BT_LANES - 1)) == 0 && k < T.rs) ys[k] = v;
+      }
+      __syncthreads();
+      b = tid < T.rs ? ys[tid] : 0.0;
+    }
+    if (reset && row >= 0) reset[row] = __longlong_as_double(SENTINEL);  // optional row reset
     if (trace) {
       __syncthreads();
       if (tid == 0) trace[6 * t + 5] = gtimer();
