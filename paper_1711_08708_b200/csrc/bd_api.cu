@@ -203,6 +203,11 @@ struct bd_system {
   double gamma;
   Ctl ctl{};
   double* tmp = nullptr;  // n+m scratch
+  // entry-major ELL copy of [S_1 | S_i] for Λ (W = 0: not built, CSR kernels)
+  int ell_w = 0;
+  int* ell_col = nullptr;
+  double* ell_v1 = nullptr;
+  double* ell_v2 = nullptr;
 };
 
 struct bd_prec {
@@ -1141,6 +1146,24 @@ bd_status inner_solve(bd_inner* p, const Rhs& rhs, double* x_int, double* out, c
 bd_status launch_lambda(bd_system* s, const double* x, double* q, const Ctl& c, int with_dot) {
   bd_ctx* ctx = s->ctx;
   const char* lv = getenv("BD_LAMBDA");
+  if (s->ell_w && !(lv && lv[0] != 'e')) {
+    const dev::LamEll L{s->ell_col, s->ell_v1, s->ell_v2};
+    const int grid = grid_for(ctx, s->n, dev::TPB);
+#define LAMBDA_ELL(WW)                                                                         \
+  case WW:                                                                                     \
+    dev::k_lambda_ell<WW><<<grid, dev::TPB, 0, ctx->stream>>>(L, x, q, s->mh, s->gamma,         \
+                                                             (int)s->n, (int)s->m, c, with_dot); \
+    break;
+    switch (s->ell_w) {
+      LAMBDA_ELL(8)
+      LAMBDA_ELL(16)
+      LAMBDA_ELL(24)
+      LAMBDA_ELL(32)
+    }
+#undef LAMBDA_ELL
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   if (!(lv && lv[0] == '1')) {
     // entries per row ~ nnz/n: 3D P1 ~15 -> 8 lanes x 2, 2D ~7 -> 4 lanes x 2
     const double avg = s->n ? (double)s->S1->nnz / s->n : 1.0;
@@ -1190,6 +1213,19 @@ bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, c
 
 bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
   bd_ctx* ctx = p->sys->ctx;
+  bd_system* sy = p->sys;
+  if (sy->ell_w && !getenv("BD_NO_CORR_ELL")) {
+    const dev::LamEll L{sy->ell_col, sy->ell_v1, sy->ell_v2};
+    const int grid = grid_for(ctx, sy->m, dev::TPB);
+    switch (sy->ell_w) {
+      case 8: dev::k_corr_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
+      case 16: dev::k_corr_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
+      case 24: dev::k_corr_ell<24><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
+      default: dev::k_corr_ell<32><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
+    }
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   {
     const double avg = p->sys->m ? (double)p->sys->Si->nnz / p->sys->m : 1.0;
     auto si2 = p->sys->Si->dev();
@@ -1522,6 +1558,36 @@ bd_status bd_system_create(bd_ctx* ctx, bd_csr* S1, bd_csr* Si, const double* ma
     return fail(ctx, BD_ECUDA, "bd_system_create: device allocation failed");
   }
   CK(ctx, cudaDeviceSynchronize());
+  // entry-major ELL copy for Λ when rows are short and near-uniform
+  {
+    std::vector<int32_t> rp(s->n + 1);
+    CK(ctx, cudaMemcpy(rp.data(), S1->dev().rowptr, sizeof(int32_t) * (s->n + 1),
+                       cudaMemcpyDeviceToHost));
+    int64_t maxlen = 0;
+    for (int64_t i = 0; i < s->n; ++i) maxlen = std::max<int64_t>(maxlen, rp[i + 1] - rp[i]);
+    const int W = maxlen <= 8 ? 8 : maxlen <= 16 ? 16 : maxlen <= 24 ? 24 : maxlen <= 32 ? 32 : 0;
+    const double fill = W && s->n ? (double)W * s->n / std::max<int64_t>(1, rp[s->n]) : 99.0;
+    if (W && fill <= 1.5 && !getenv("BD_NO_LAMBDA_ELL")) {
+      int* bad = nullptr;
+      if (dalloc(&s->ell_col, (int64_t)W * s->n) || dalloc(&s->ell_v1, (int64_t)W * s->n) ||
+          dalloc(&s->ell_v2, (int64_t)W * s->m) || dalloc(&bad, 1) || cudaMemset(bad, 0, sizeof(int)))
+        return fail(ctx, BD_ECUDA, "bd_system_create: ELL allocation failed");
+      dev::k_build_lambda_ell<<<(int)((s->n + 255) / 256), 256>>>(
+          S1->dev(), Si->dev(), (int)s->n, (int)s->m, W, s->ell_col, s->ell_v1, s->ell_v2, bad);
+      int hb = 0;
+      CK(ctx, cudaMemcpy(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost));
+      cudaFree(bad);
+      if (hb) {
+        cudaFree(s->ell_col);
+        cudaFree(s->ell_v1);
+        cudaFree(s->ell_v2);
+        s->ell_col = nullptr;
+        s->ell_v1 = s->ell_v2 = nullptr;
+      } else {
+        s->ell_w = W;
+      }
+    }
+  }
   // ΣM once, fixed order (bd/system.py:145 denominator)
   {
     Scope sc(ctx);
@@ -1539,6 +1605,9 @@ bd_status bd_system_destroy(bd_system* s) {
   cudaFree(s->mass);
   cudaFree(s->mh);
   cudaFree(s->tmp);
+  cudaFree(s->ell_col);
+  cudaFree(s->ell_v1);
+  cudaFree(s->ell_v2);
   ctl_free(&s->ctl);
   delete s;
   return BD_OK;

@@ -364,6 +364,99 @@ __global__ void __launch_bounds__(TPB) k_lambda(Csr s1, Csr si, const double* __
 // Λ with K entries per lane: the S_1 and S_i entries of a row are loaded, and
 // their operands gathered, before any reduction (two memory round trips per
 // row instead of four).  Rows longer than G*K fall back to a loop.
+// ---- Λ on an entry-major ELL copy of the blocks ------------------------------
+// One thread per row; S_1 and S_i share the column array (pattern(S_i) is a
+// subset of the heart rows of pattern(S_1); absent / padding entries are 0).
+// Entry e of row r sits at [e * rows + r], so every load of a warp is one
+// contiguous 128/256-byte request, and all of a row's loads are independent.
+struct LamEll {
+  const int* col;     // [W][n]  (padding: the row itself)
+  const double* v1;   // [W][n]  S_1
+  const double* v2;   // [W][m]  S_i on heart rows
+};
+
+__global__ void k_build_lambda_ell(Csr s1, Csr si, int n, int m, int W, int* __restrict__ col,
+                                   double* __restrict__ v1, double* __restrict__ v2,
+                                   int* __restrict__ bad) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int b1 = s1.rowptr[row], e1 = s1.rowptr[row + 1];
+  if (e1 - b1 > W) {
+    atomicExch(bad, 1);
+    return;
+  }
+  int b2 = 0, e2 = 0;
+  if (row < m) {
+    b2 = si.rowptr[row];
+    e2 = si.rowptr[row + 1];
+  }
+  int j = b2;
+  for (int e = 0; e < W; ++e) {
+    const int k = b1 + e;
+    const int cc = k < e1 ? s1.col[k] : row;
+    col[(size_t)e * n + row] = cc;
+    v1[(size_t)e * n + row] = k < e1 ? s1.val[k] : 0.0;
+    if (row < m) {
+      double a = 0.0;
+      if (k < e1 && j < e2 && si.col[j] == cc) a = si.val[j++];
+      v2[(size_t)e * m + row] = a;
+    }
+  }
+  if (j != e2) atomicExch(bad, 1);  // an S_i entry outside the S_1 pattern (or unsorted)
+}
+
+template <int W>
+__global__ void __launch_bounds__(TPB) k_lambda_ell(LamEll L, const double* __restrict__ x,
+                                                    double* __restrict__ q,
+                                                    const double* __restrict__ mh, double gamma,
+                                                    int n, int m, Ctl c, int with_dot) {
+  if (inactive(c)) return;
+  __shared__ double sm[32];
+  const double* __restrict__ u = x;
+  const double* __restrict__ v = x + n;
+  double acc = 0.0;
+  for (int row = blockIdx.x * TPB + threadIdx.x; row < n; row += gridDim.x * TPB) {
+    const bool h = row < m;
+    double s_top = 0.0, su = 0.0, sv = 0.0;
+#pragma unroll
+    for (int e0 = 0; e0 < W; e0 += 8) {
+      int cl[8];
+      double a1[8], a2[8], xu[8], xv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cl[e] = __ldg(&L.col[(size_t)(e0 + e) * n + row]);
+        a1[e] = __ldg(&L.v1[(size_t)(e0 + e) * n + row]);
+        a2[e] = h ? __ldg(&L.v2[(size_t)(e0 + e) * m + row]) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xu[e] = __ldg(&u[cl[e]]);
+        xv[e] = (h && cl[e] < m) ? __ldg(&v[cl[e]]) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        s_top = fma(a1[e], xu[e], s_top);
+        su = fma(a2[e], xu[e], su);
+        sv = fma(a2[e], xv[e], sv);
+      }
+    }
+    double top = s_top;
+    if (h) {
+      top = __dadd_rn(top, sv);
+      const double vi = v[row];
+      const double bot = __dadd_rn(__dadd_rn(su, sv), __dmul_rn(gamma, __dmul_rn(mh[row], vi)));
+      q[n + row] = bot;
+      acc = fma(vi, bot, acc);
+    }
+    q[row] = top;
+    acc = fma(u[row], top, acc);
+  }
+  if (with_dot) {
+    double vv[1] = {block_sum(acc, sm)};
+    reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_LAMBDA, FIN_DQ, 0, -1, 0, sm);
+  }
+}
+
 template <int G, int K>
 __global__ void __launch_bounds__(TPB) k_lambda2(Csr s1, Csr si, const double* __restrict__ x,
                                                  double* __restrict__ q,
@@ -2070,6 +2163,36 @@ __global__ void __launch_bounds__(TPB) k_corr2(Csr si, const double* __restrict_
   }
   double vv[1] = {block_sum(acc, sm)};
   reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_CORR, FIN_MEAN, S_MU2, S_C2, n, sm);
+}
+
+// corr = S_i s on the ELL copy (thread per heart row), + its sum for mu2.
+template <int W>
+__global__ void __launch_bounds__(TPB) k_corr_ell(LamEll L, int n, int m, const double* __restrict__ s,
+                                                  double* __restrict__ corr, Ctl c, int64_t nmean) {
+  if (inactive(c)) return;
+  __shared__ double sm[32];
+  double acc = 0.0;
+  for (int r = blockIdx.x * TPB + threadIdx.x; r < m; r += gridDim.x * TPB) {
+    double v = 0.0;
+#pragma unroll
+    for (int e0 = 0; e0 < W; e0 += 8) {
+      int cl[8];
+      double a[8], xv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cl[e] = __ldg(&L.col[(size_t)(e0 + e) * n + r]);
+        a[e] = __ldg(&L.v2[(size_t)(e0 + e) * m + r]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) xv[e] = cl[e] < m ? __ldg(&s[cl[e]]) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v = fma(a[e], xv[e], v);
+    }
+    corr[r] = v;
+    acc += v;
+  }
+  double vv[1] = {block_sum(acc, sm)};
+  reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_CORR, FIN_MEAN, S_MU2, S_C2, nmean, sm);
 }
 
 // z_u = t - bulk(corr) with both recentrings applied on the fly
