@@ -840,8 +840,12 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
     }
     const int x0 = bs.tile_in_ptr[t], nx = bs.tile_in_ptr[t + 1] - x0;
     for (int j = 0; j < nx; ++j) in[(size_t)t * xs + j] = bs.in_col[x0 + j];
-    const int64_t i0 = bs.tile_inv_ptr[t], ni = bs.tile_inv_ptr[t + 1] - i0;
-    std::copy(bs.inv.begin() + i0, bs.inv.begin() + i0 + ni, inv.begin() + (size_t)t * is);
+    // packed row-major (k(k+1)/2 + l) -> packed column-major (l*n - l(l-1)/2 + k - l)
+    const int64_t i0 = bs.tile_inv_ptr[t];
+    for (int k = 0; k < n_; ++k)
+      for (int l = 0; l <= k; ++l)
+        inv[(size_t)t * is + (size_t)l * n_ - (size_t)l * (l - 1) / 2 + (k - l)] =
+            bs.inv[i0 + (int64_t)k * (k + 1) / 2 + l];
   }
   CK(ctx, upload_vec(&out->tile_nr, nr));
   CK(ctx, upload_vec(&out->task_row, row));

@@ -1529,9 +1529,12 @@ constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
 __host__ __device__ constexpr int bt_even(int v) { return (v + 1) & ~1; }
 __host__ __device__ constexpr int bt_round8(int v) { return (v + 7) & ~7; }
-// shared-memory layout (bytes) of one tile: ys | xin | inv | ent_val | ent_slot | ent_rp
+// shared-memory layout (bytes) of one tile:
+// partials[256] | ys | xin | inv | ent_val | ent_slot | ent_rp
+constexpr int BT_PART = 256;
 __host__ __device__ constexpr size_t bt_smem(int rs, int xs, int is, int es, int rps) {
-  return sizeof(double) * ((size_t)rs + xs + is + es) + sizeof(unsigned short) * ((size_t)es + rps);
+  return sizeof(double) * ((size_t)BT_PART + rs + xs + 2 + is + 2 + es) +
+         sizeof(unsigned short) * ((size_t)es + rps);
 }
 
 template <class Rhs>
@@ -1540,22 +1543,31 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
                                                     double* __restrict__ reset) {
   if (inactive(c)) return;
   extern __shared__ __align__(16) double bt_sm[];
-  double* ys = bt_sm;         // rs
-  double* xin = ys + T.rs;    // xs external inputs
-  double* is = xin + T.xs;    // packed inverse
-  double* ev = is + T.is;     // external entries
+  double* part = bt_sm;              // dense partials [G][R], G*R <= BT_PART
+  double* ys = part + BT_PART;       // rs
+  double* xin = ys + T.rs;           // xs external inputs
+  double* is = xin + T.xs + 2;       // inverse, packed column-major: column l = rows l..nr-1
+  double* ev = is + T.is + 2;        // external entries (is[T.is] = 0: zero slot)
   unsigned short* esl = reinterpret_cast<unsigned short*>(ev + T.es);
   unsigned short* erp = esl + T.es;
   __shared__ int task_s;
   __shared__ int last_s;
   const int tid = threadIdx.x, nth = blockDim.x;
+  // dense step mapping: G column groups x R rows (R = rs rounded to 32)
+  const int R = (T.rs + 31) & ~31;
+  const int G = max(1, nth / R);
+  const int kk = tid % R, gg = tid / R;
+  if (tid == 0) {  // zero slots (never overwritten: copies stop short of them)
+    is[T.is] = 0.0;
+    xin[T.xs] = 0.0;
+  }
   for (;;) {
     if (tid == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
     __syncthreads();
     const int t = task_s;
     if (t >= T.ntiles) break;
     unsigned long long* trace = g_tile_trace;
-    if (trace && tid == 0) trace[6 * t] = gtimer();
+    if (trace && tid == 0) trace[8 * t] = gtimer();
     if (tid == 0 && T.prefetch && t + (int)gridDim.x < T.ntiles) {
       const int u = t + (int)gridDim.x;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(T.inv + (int64_t)u * T.is),
@@ -1570,17 +1582,17 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
       const int j = tid + h * nth;
       icol[h] = j < T.xs ? T.in_col[(int64_t)t * T.xs + j] : -1;
     }
-    // inverse block and external entries -> smem (independent of x)
-    {
-      const int ninv = bt_even(nr * (nr + 1) / 2);
-      const double* ib = T.inv + (int64_t)t * T.is;
-      for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is + 2 * q, ib + 2 * q);
+    {  // group 1: external entries (small); group 2: the inverse
       const double* vb = T.ent_val + (int64_t)t * T.es;
       for (int q = tid; 2 * q < T.es; q += nth) cp_async16(ev + 2 * q, vb + 2 * q);
       const unsigned short* sb = T.ent_slot + (int64_t)t * T.es;
       for (int q = tid; 8 * q < T.es; q += nth) cp_async16(esl + 8 * q, sb + 8 * q);
       const unsigned short* rb = T.ent_rp + (int64_t)t * T.rps;
       for (int q = tid; 8 * q < T.rps; q += nth) cp_async16(erp + 8 * q, rb + 8 * q);
+      cp_async_commit();
+      const int ninv = bt_even(nr * (nr + 1) / 2);
+      const double* ib = T.inv + (int64_t)t * T.is;
+      for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is + 2 * q, ib + 2 * q);
       cp_async_commit();
     }
     double b;
@@ -1601,7 +1613,7 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
     if (reset && row >= 0) reset[row] = __longlong_as_double(SENTINEL);  // optional row reset
     if (trace) {
       __syncthreads();
-      if (tid == 0) trace[6 * t + 5] = gtimer();
+      if (tid == 0) trace[8 * t + 5] = gtimer();
     }
     // the tile's distinct inputs: one poller each
 #pragma unroll
@@ -1622,47 +1634,71 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
     }
     cp_async_wait<0>();
     __syncthreads();
-    if (trace && tid == 0) trace[6 * t + 4] = gtimer();
-    if (row >= 0) {
+    if (trace && tid == 0) trace[8 * t + 4] = gtimer();
+    // y_k = b_k - sum_ext: branch-free (padding entries read the zero input
+    // slot xin[xs] with a zero-padded value)
+    if (tid < T.rs) {
+      const int e0 = erp[tid], e1 = erp[tid + 1];
+      int sl[8];
+      double vl[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = e0 + e < e1;
+        const int ei = ok ? e0 + e : 0;
+        sl[e] = ok ? (int)esl[ei] : T.xs;
+        vl[e] = ev[ei];
+      }
       double acc = 0.0;
-      const int e1 = erp[tid + 1];
-      for (int e = erp[tid]; e < e1; ++e) acc = fma(ev[e], xin[esl[e]], acc);
-      ys[tid] = __dsub_rn(b, acc);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fma(vl[e], xin[sl[e]], acc);
+      ys[tid] = row >= 0 ? __dsub_rn(b, acc) : 0.0;
     }
+    if (trace && tid == 0) trace[8 * t + 6] = gtimer();
     __syncthreads();
-    if (trace && tid == 0) trace[6 * t + 1] = gtimer();
-    // x_k = sum_{l<=k} inv[k][l] y_l
-    const int q = tid & (BT_LANES - 1);
-    for (int base = 0; base < nr; base += nth / BT_LANES) {
-      const int k = base + tid / BT_LANES;
-      double s = 0.0;
-      if (k < nr) {
-        // 16 entries per lane per round: all shared loads issued before the FMAs
-        const double* ik = is + (k * (k + 1) >> 1);
-        double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int l0 = q; l0 <= k; l0 += 16 * BT_LANES) {
-          double a[16], yv[16];
+    if (trace && tid == 0) trace[8 * t + 1] = gtimer();
+    // x_k = sum_g sum_{l in group g, l <= k} inv[k][l] y_l ; column l of the
+    // packed column-major inverse starts at l*nr - l*(l-1)/2
+    {
+      const int L = (nr + G - 1) / G;
+      const int l0 = gg * L;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (gg < G && kk < nr) {
+        // no conditional loads (they compile to branches that serialise the
+        // shared-memory pipeline): out-of-range lanes read the zero slot
+        // is[T.is] and a valid y; column offsets advance incrementally,
+        // idx(l+1) = idx(l) + nr - l - 1
+        const int zero = T.is;
+        int l = l0;
+        int idx = l * nr - ((l * (l - 1)) >> 1) + (kk - l);
+        const int lend = min(l0 + L, kk + 1);
+        for (int u0 = l0; u0 < lend; u0 += 16) {
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
-            const int l = l0 + u * BT_LANES;
-            a[u] = l <= k ? ik[l] : 0.0;
-            yv[u] = l <= k ? ys[l] : 0.0;
+            const bool ok = l < lend;
+            const double av = is[ok ? idx : zero];
+            const double yy = ys[ok ? l : 0];
+            s4[u & 3] = fma(av, yy, s4[u & 3]);
+            idx += nr - l - 1;
+            ++l;
           }
-#pragma unroll
-          for (int u = 0; u < 16; ++u) s4[u & 3] = fma(a[u], yv[u], s4[u & 3]);
         }
-        s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
-#pragma unroll
-      for (int o = 1; o < BT_LANES; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (q == 0 && k < nr) publish(&xg[T.task_row[(int64_t)t * T.rs + k]], s);
+      const double sp = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      if (gg < G) part[gg * R + kk] = sp;
     }
+    __syncthreads();
+    if (tid < nr) {
+      double x = part[tid];
+      for (int g = 1; g < G; ++g) x += part[g * R + tid];
+      publish(&xg[row], x);
+    }
+    if (trace && tid == 0) trace[8 * t + 7] = gtimer();
     __syncthreads();  // smem reuse by the next tile
     if (trace && tid == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      trace[6 * t + 2] = gtimer();
-      trace[6 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
+      trace[8 * t + 2] = gtimer();
+      trace[8 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
     }
   }
   if (tid == 0) {

@@ -29,7 +29,7 @@ V = wl.mesh.vertices
 rank = [np.searchsorted(np.unique(V[:, a]), V[first, a]) for a in range(3)]
 bins = np.stack([r // 4 for r in rank], 1)
 key = {tuple(b): t for t, b in enumerate(bins)}
-buf = torch.zeros(nt * 6 + 8, dtype=torch.int64, device='cuda')
+buf = torch.zeros(nt * 8 + 8, dtype=torch.int64, device='cuda')
 y = torch.as_tensor(np.random.default_rng(0).standard_normal(g.shape[0])).cuda()
 for _ in range(3):
     inner.apply_inverse(y)
@@ -39,10 +39,11 @@ for rep in range(reps):
     L.bd_debug_tile_trace(C.c_void_p(buf.data_ptr()), 1)
     inner.apply_inverse(y); torch.cuda.synchronize()
     L.bd_debug_tile_trace(None, 0)
-    tr = buf[: nt * 6].view(nt, 6).cpu().numpy().astype(np.int64)
+    tr = buf[: nt * 8].view(nt, 8).cpu().numpy().astype(np.int64)
     t0 = tr[:, 0].min()
     grab, ready, done = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
     polled, prep = (tr[:, 4] - t0) / 1e3, (tr[:, 5] - t0) / 1e3
+    extd, densed = (tr[:, 6] - t0) / 1e3, (tr[:, 7] - t0) / 1e3
     deps = []
     for t in range(nt):
         b = bins[t]
@@ -73,6 +74,14 @@ for rep in range(reps):
     print(f"   path: poll-after-max(dep,prep) sum {p_poll.sum():.1f} median {np.median(p_poll):.2f}; "
           f"polled->ready sum {p_cp.sum():.1f} median {np.median(p_cp):.2f}; grab->prep median {np.median(p_prep):.2f}; "
           f"prep after last dep: {(prep[path] > last_dep[path]).sum()} tiles")
+    P = np.array(path)
+    print("   path medians: ext-sum %.2f, sync %.2f, dense %.2f, tail(sync) %.2f" % (
+        np.median(extd[P] - polled[P]), np.median(ready[P] - extd[P]), np.median(densed[P] - ready[P]),
+        np.median(done[P] - densed[P])))
+    dn = densed - ready
+    order = np.argsort(ready)
+    print("   dense by start order (first 50 / middle / last 50 tiles): %.2f / %.2f / %.2f" % (
+        np.median(dn[order[:50]]), np.median(dn[order[len(order)//2-500:len(order)//2+500]]), np.median(dn[order[-50:]])))
     seg = np.array_split(np.arange(len(path)), 6)
     print("   path poll/cp by segment:", [(round(p_poll[s_].mean(), 2), round(p_cp[s_].mean(), 2)) for s_ in seg])
     print("   path hop/compute by segment:", [(round(ph[s].mean(), 2), round(pc[s].mean(), 2)) for s in seg])
