@@ -483,7 +483,7 @@ def run_reference(args, rank):
     total = float(np.sum(step_times))
     value = args.steps / total if total > 0 else None
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6) if value else None,
-            "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * total / args.steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic structured mesh)",
