@@ -360,6 +360,7 @@ def run_sharded(args, rank, world, local_rank):
     for _ in range(args.steps):
         state, st = sim.step(state)
         iters.append(st["iterations"])
+    graph_used, graph_err = st.get("graph"), st.get("graph_error")
     e1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -383,6 +384,7 @@ def run_sharded(args, rank, world, local_rank):
                        "dof": n + m, "raw_steps_per_s": round(steps_s, 4),
                        "value_definition": "steps/s x dof / dof(cfg2): cfg2-equivalent steps/s",
                        "pcg_iters_per_step": round(float(np.mean(iters)), 2),
+                       "pcg_loop": "cuda graph" if graph_used else f"eager ({graph_err})",
                        "parallelism": f"mesh partition x{world}"},
             "gpu_launches": int(ctx.launches() - launches0), "clocks": clk,
             "setup_s": round(t_setup, 1)}), flush=True)
@@ -513,10 +515,12 @@ def main():
     ap.add_argument("--inner", default=None)
     ap.add_argument("--cpu-iters", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", default=os.environ.get("BD_BENCH_MODE", "replicas"),
+    ap.add_argument("--mode", default=os.environ.get("BD_BENCH_MODE"),
                     choices=["replicas", "sharded"],
-                    help="N>1: independent replicas of cfg2 per GPU, or the mesh sharded "
-                         "across GPUs (weak scaling, 8 GPUs = config 3)")
+                    help="N>1 default 'sharded': the slab partitioned across the GPUs (RCB, "
+                         "NCCL halo + all-reduce; weak scaling, 8 GPUs = config 3); 'replicas': "
+                         "N independent cfg2 solves.  N=1 runs the single-graph cfg2 solve "
+                         "unless --mode sharded is given.")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -529,6 +533,8 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.mode is None:
+        args.mode = "sharded" if world > 1 else "replicas"
     if args.mode == "sharded":
         if world == 1:
             import torch

@@ -141,25 +141,44 @@ def build_local(S1, Si, mass, heart_mass, gamma, grounded, Km, part: np.ndarray,
 
 # ---- communication -------------------------------------------------------------------
 class Comm:
-    """torch.distributed wrapper: halo exchange and global sums."""
+    """torch.distributed wrapper: halo exchange and global sums.
+
+    Nothing here reads a value back to the host: sums are all-reduced in place
+    on device tensors (NCCL on the box, gloo in the CPU tests) and the halo
+    index lists are uploaded once."""
 
     def __init__(self, dist, device):
         self.dist = dist
         self.device = device
+        self._idx = {}
 
     def allreduce(self, vals):
+        """Host list -> host list (setup only: synchronises)."""
         torch = _torch()
         t = torch.tensor(vals, dtype=torch.float64, device=self.device)
         self.dist.all_reduce(t)
         return t.tolist()
 
-    def halo(self, x_own, send: dict, recv: dict, nslots: int):
+    def allreduce_(self, t):
+        """In-place global sum of a device tensor (no host round trip)."""
+        self.dist.all_reduce(t)
+        return t
+
+    def _index(self, key, idx):
+        torch = _torch()
+        t = self._idx.get(key)
+        if t is None:
+            t = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=self.device)
+            self._idx[key] = t
+        return t
+
+    def halo(self, x_own, send: dict, recv: dict, nslots: int, tag: str = ""):
         """Ghost values of x from the owning neighbours (one layer)."""
         torch = _torch()
         out = torch.zeros(nslots, dtype=x_own.dtype, device=x_own.device)
         ops, bufs = [], {}
         for q, idx in send.items():
-            buf = x_own[torch.as_tensor(idx, device=x_own.device)].contiguous()
+            buf = x_own.index_select(0, self._index((tag, "s", q), idx))
             ops.append(self.dist.P2POp(self.dist.isend, buf, q))
         for q, slots in recv.items():
             bufs[q] = torch.empty(len(slots), dtype=x_own.dtype, device=x_own.device)
@@ -168,7 +187,7 @@ class Comm:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
         for q, slots in recv.items():
-            out[torch.as_tensor(slots, device=x_own.device)] = bufs[q]
+            out.index_copy_(0, self._index((tag, "r", q), slots), bufs[q])
         return out
 
 
@@ -201,7 +220,7 @@ class DistributedSystem:
 
     def ext_u(self, u):
         lp = self.lp
-        g = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size)
+        g = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size, "u")
         return _torch().cat([u, g]), g
 
     def ext_heart(self, v_own, ghost_heart):
@@ -209,7 +228,7 @@ class DistributedSystem:
 
     def heart_ghosts(self, v):
         lp = self.lp
-        return self.comm.halo(v, lp.send_heart, lp.recv_heart, lp.m_ghost)
+        return self.comm.halo(v, lp.send_heart, lp.recv_heart, lp.m_ghost, "h")
 
     def apply(self, x):
         """q = Λ x (bd/system.py:106-116) with halo exchanges of u and v."""
@@ -225,15 +244,22 @@ class DistributedSystem:
         bottom = iu + iv + lp.gamma * (self.mh * v)
         return _torch().cat([top, bottom])
 
+    def dot_t(self, a, b):
+        """Global a·b as a device 0-d tensor."""
+        return self.comm.allreduce_((a * b).sum().reshape(1))[0]
+
+    def mean_u_t(self, u):
+        return self.comm.allreduce_(u.sum().reshape(1))[0] / self.lp.n_global
+
     def dot(self, a, b):
-        return self.comm.allreduce([float((a * b).sum())])[0]
+        return float(self.dot_t(a, b))
 
     def mean_u(self, u):
-        return self.comm.allreduce([float(u.sum())])[0] / self.lp.n_global
+        return float(self.mean_u_t(u))
 
     def normalize(self, x):
         lp = self.lp
-        alpha = self.comm.allreduce([float((self.mass * x[: lp.n_own]).sum())])[0] / self.msum
+        alpha = self.comm.allreduce_((self.mass * x[: lp.n_own]).sum().reshape(1))[0] / self.msum
         out = x.clone()
         out[: lp.n_own] -= alpha
         return out
@@ -245,16 +271,18 @@ class DistributedBlockLU:
     def __init__(self, dsys: DistributedSystem, inner: str, beta: float):
         self.s, self.beta = dsys, beta
         be = dsys.be
-        self.bulk = be.inner(inner, dsys.lp.bulk_block)
-        self.schur = be.inner(inner, dsys.lp.schur_block)
+        lp = dsys.lp
+        xyz = getattr(lp, "coords", None)  # owned-vertex coordinates: lattice tiles for IC(0)
+        self.bulk = be.inner(inner, lp.bulk_block, None if xyz is None else xyz)
+        self.schur = be.inner(inner, lp.schur_block, None if xyz is None else xyz[: lp.m_own])
         self.p1 = self.pk = self.si = 0
 
     def bulk_inverse(self, y):
         self.p1 += 1
         s = self.s
-        mean = s.mean_u(y)
+        mean = s.mean_u_t(y)
         z = s.be.inner_apply(self.bulk, y - mean)
-        z = z - s.mean_u(z)
+        z = z - s.mean_u_t(z)
         return z + mean / self.beta
 
     def apply(self, r):
@@ -274,14 +302,22 @@ class DistributedBlockLU:
 
 
 def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e-6,
-                    max_iter=500, x0=None):
-    """The reference iteration (bd/krylov.py:46-140) on the sharded system.
-    Returns (x_local, stats dict); raises RuntimeError past max_iter / breakdown."""
+                    max_iter=500, x0=None, check_every=16, graph=None):
+    """The reference iteration (bd/krylov.py:46-140) on the sharded system,
+    device-resident: every scalar (α, β, ρ, the means, the residual) stays a
+    device tensor, reductions are in-place all-reduces, and the host reads the
+    convergence / breakdown flags only every `check_every` iterations.
+    Iterations after convergence are masked to exact no-ops (α = 0, ρ and d
+    kept), so iterates, histories and counts equal those of the per-iteration
+    test.  On a CUDA device one iteration is captured into a CUDA graph (NCCL
+    collectives included) and replayed; `graph=False` (or a failed capture)
+    runs the same body eagerly.  Returns (x_local, stats dict); raises
+    RuntimeError past max_iter / on breakdown (bd/krylov.py:103-108, 133-135)."""
+    torch = _torch()
     st = {"iterations": 0, "residual_history": [], "preconditioned_history": [],
           "mv_count": 0, "converged": False}
     n = dsys.n
-    nb = dsys.dot(b, b) ** 0.5
-    torch = _torch()
+    nb = float(dsys.dot_t(b, b)) ** 0.5
     if nb == 0.0:
         st["residual_history"].append(0.0)
         st["converged"] = True
@@ -293,7 +329,7 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
         x = x0.clone()
         r = b - dsys.apply(x)
     st["mv_count"] += 1
-    rel = dsys.dot(r, r) ** 0.5 / nb
+    rel = float(dsys.dot_t(r, r)) ** 0.5 / nb
     st["residual_history"].append(rel)
     if rel <= tol:
         st["converged"] = True
@@ -301,37 +337,97 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
 
     def precond(r):
         z = prec.apply(r)
-        z[:n] -= dsys.mean_u(z[:n])  # _deflate
+        z[:n] -= dsys.mean_u_t(z[:n])  # _deflate
         return z
 
+    dev, f64 = b.device, torch.float64
+    cnt = [prec.p1, prec.pk, prec.si]
     z = precond(r)
-    rho = dsys.dot(r, z)
-    st["preconditioned_history"].append(rho)
-    d = z.clone()
-    for _ in range(max_iter):
+    S = {  # static state of the loop (graph-safe: only updated in place)
+        "x": x, "r": r, "d": z.clone(),
+        "rho": dsys.dot_t(r, z).reshape(()).clone(),
+        "active": torch.ones((), dtype=torch.bool, device=dev),
+        "bad": torch.zeros((), dtype=torch.bool, device=dev),
+        "iters": torch.zeros((), dtype=torch.int64, device=dev),
+        "k": torch.zeros((), dtype=torch.int64, device=dev),
+        "res": torch.full((max_iter + 1,), -1.0, dtype=f64, device=dev),
+        "pre": torch.full((max_iter + 1,), float("nan"), dtype=f64, device=dev),
+    }
+    S["pre"][0] = S["rho"]
+    zero = torch.zeros((), dtype=f64, device=dev)
+
+    def body():
+        d, rho, active = S["d"], S["rho"], S["active"]
         q = dsys.apply(d)
-        st["mv_count"] += 1
-        dq = dsys.dot(d, q)
-        if not np.isfinite(dq) or dq <= 0.0:
-            raise RuntimeError(f"conjugate gradient breakdown: curvature {dq}")
-        alpha = rho / dq
-        x = x + alpha * d
-        r = r - alpha * q
-        st["iterations"] += 1
-        rel = dsys.dot(r, r) ** 0.5 / nb
-        st["residual_history"].append(rel)
-        if rel <= tol:
-            st["converged"] = True
-            break
-        z = precond(r)
-        rho_next = dsys.dot(r, z)
-        st["preconditioned_history"].append(rho_next)
-        beta = rho_next / rho
-        rho = rho_next
-        d = z + beta * d
-    if not st["converged"]:
+        dq = dsys.dot_t(d, q)
+        brk = active & ~(torch.isfinite(dq) & (dq > 0))
+        S["bad"].logical_or_(brk)
+        go = active & ~brk
+        alpha = torch.where(go, rho / dq, zero)
+        S["x"].add_(alpha * d)
+        S["r"].sub_(alpha * q)
+        S["iters"].add_(go.to(torch.int64))
+        relk = torch.sqrt(dsys.dot_t(S["r"], S["r"])) / nb
+        S["k"].add_(1)
+        S["res"].index_put_((S["k"],), torch.where(go, relk, torch.full_like(relk, -1.0)))
+        act = go & ~(relk <= tol)
+        zz = precond(S["r"])
+        rho_next = dsys.dot_t(S["r"], zz)
+        S["pre"].index_put_((S["k"],), torch.where(act, rho_next, torch.full_like(rho_next, float("nan"))))
+        beta = torch.where(act, rho_next / rho, zero)
+        d.copy_(torch.where(act, zz + beta * d, d))
+        rho.copy_(torch.where(act, rho_next, rho))
+        active.copy_(act)
+
+    use_graph = graph if graph is not None else (dev.type == "cuda")
+    g = None
+    k_done = 0
+    if use_graph:
+        from . import _lib
+        ctx = _lib.Context.default()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # first iteration eagerly: warms the allocator pools
+            ctx.sync_stream()
+            body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        k_done = 1
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                ctx.sync_stream()
+                body()
+        except Exception as e:  # capture unsupported here (e.g. P2P in capture): eager body
+            g = None
+            st["graph_error"] = f"{type(e).__name__}: {e}"[:300]
+        ctx.sync_stream()
+    while k_done < max_iter:
+        if g is not None:
+            g.replay()
+        else:
+            body()
+        k_done += 1
+        if k_done % check_every == 0 or k_done == max_iter:
+            if not bool(S["active"]) or bool(S["bad"]):
+                break
+    n_it = int(S["iters"])
+    # the reference applies P^-1 once before the loop and once per
+    # non-final iteration (bd/krylov.py:95, 125): p1 += 2, pk += 1, si += 2 each
+    prec.p1, prec.pk, prec.si = cnt[0] + 2 * n_it, cnt[1] + n_it, cnt[2] + 2 * n_it
+    bad = bool(S["bad"])
+    res = S["res"][1: k_done + 1].tolist()
+    st["residual_history"].extend(h for h in res if h >= 0)
+    pre = S["pre"][: k_done + 1].tolist()
+    st["preconditioned_history"] = [h for h in pre if h == h]
+    st["iterations"] = n_it
+    st["graph"] = g is not None
+    st["mv_count"] += n_it + (1 if bad else 0)
+    if bad:
+        raise RuntimeError("conjugate gradient breakdown: curvature <= 0 or not finite")
+    if bool(S["active"]):
         raise RuntimeError(f"PCG did not reach tol={tol} within {max_iter} iterations")
-    return dsys.normalize(x), st
+    st["converged"] = True
+    return dsys.normalize(S["x"]), st
 
 
 class NativeBackend:
@@ -351,11 +447,14 @@ class NativeBackend:
     def spmv(self, h, x):
         return h.matvec(x.contiguous())
 
-    def inner(self, kind, a):
+    def inner(self, kind, a, coords=None):
         from .precond import make_inner
 
         p = make_inner(kind)
-        p.setup(a)
+        if coords is not None and hasattr(p, "setup") and kind == "ic0":
+            p.setup(a, coords=coords)
+        else:
+            p.setup(a)
         return p
 
     def inner_apply(self, h, y):
@@ -485,6 +584,7 @@ def build_local_from_mesh(mesh, params, fibers, dt, part: np.ndarray, rank: int,
             if hm.any():
                 lp.recv_heart[q] = g2l[mine[hm]] - owned.size
     lp.beta = beta
+    lp.coords = np.ascontiguousarray(mesh.vertices[owned], dtype=float)
     return lp
 
 

@@ -26,7 +26,7 @@ class ScipyBackend:
         import torch
         return torch.as_tensor(a @ x.numpy())
 
-    def inner(self, kind, a):
+    def inner(self, kind, a, coords=None):
         from oracle import bidomain_oracle as orc
         return orc.make_inner(kind, a)
 
