@@ -166,3 +166,38 @@ def test_builders_and_assembly_bit_identical_to_reference():
         kr = R.build_monodomain_matrix(mr, R.default_params(d), sr.gamma)
         kb = bd.build_monodomain_matrix(mb, bd.default_params(d), sb.gamma)
         assert np.array_equal(kr.data, kb.data)
+
+
+def _hostcheck(src, out, *args):
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    exe = os.path.join("/tmp", out)
+    subprocess.run([gxx, "-O2", "-std=c++17", os.path.join(root, "tools", "hostcheck", src),
+                    os.path.join(root, "paper_1711_08708_b200", "csrc", "bd_host.cpp"), "-o", exe],
+                   check=True, capture_output=True)
+    return subprocess.run([exe, *args], check=True, capture_output=True, text=True).stdout
+
+
+def test_btile_schedule_host():
+    """Blocked-tile schedules (bd::build_btile_schedule): every external input
+    of a tile lies in an earlier tile, and a pass simulated tile by tile
+    (y = b - L_ext x; x = inv(L_TT) y) equals plain substitution (fwd and bwd)."""
+    out = _hostcheck("btile_check.cpp", "bd_btile_check")
+    assert out.strip().endswith("OK"), out
+
+
+def test_lattice_tiles_depth():
+    """bd::partition_grid on the cfg2 lattice: 64-row tiles give a tile DAG of
+    depth 81 (= 33 + 33 + 17 - 2), against >200 for coordinate bisection."""
+    out_grid = _hostcheck("tile_depth.cpp", "bd_tile_depth", "129", "129", "65", "64", "1")
+    out_rcb = _hostcheck("tile_depth.cpp", "bd_tile_depth", "129", "129", "65", "64", "0")
+    import re
+    dg = int(re.search(r"tile-DAG depth (\d+)", out_grid).group(1))
+    dr = int(re.search(r"tile-DAG depth (\d+)", out_rcb).group(1))
+    assert dg == 81, out_grid
+    assert dr > 2 * dg, out_rcb
