@@ -11,7 +11,7 @@ import pytest
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
-from conftest import csr, golden
+from conftest import REPO, csr, golden
 
 from paper_1711_08708_b200 import distributed as D
 
@@ -164,3 +164,18 @@ def test_local_assembly_matches_global():
             assert np.array_equal(ref.recv[q], loc.recv[q])
         for q in ref.send_heart:
             assert np.array_equal(ref.send_heart[q], loc.send_heart[q])
+
+
+def test_weak_scaling_grids():
+    """bench.py --mode sharded refines the cfg2 slab so every rank keeps a
+    cfg2-sized part; 8 ranks is exactly BASELINE config 3 (256x256x128)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(REPO, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    base = (128, 128, 64)
+    assert b.weak_cells(base, 1) == base
+    assert b.weak_cells(base, 8) == (256, 256, 128)
+    for w in (1, 2, 4, 8, 16):
+        c = b.weak_cells(base, w)
+        assert c[0] * c[1] * c[2] == w * base[0] * base[1] * base[2]
