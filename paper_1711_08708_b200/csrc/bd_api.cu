@@ -143,12 +143,16 @@ struct DevBTile {
   int* in_col = nullptr;
   double* inv = nullptr;
   int ntiles = 0, rs = 0, xs = 0, is = 0, es = 0, rps = 0, grid = 0, threads = 256, sleep_ns = 0,
-      prefetch = 1;
+      prefetch = 1, poll_depth = 3;
   size_t smem = 0;
+  bool pipe = false;      // k_trsv_ptile (pipelined; needs opos / tile-ordered rhs)
+  int* opos = nullptr;    // forward schedule: slot of each row in the backward tile order
+  bool reg = false;       // k_trsv_rtile instead of k_trsv_btile
+  bool reg_smem = false;  // k_trsv_rtile with the inverse staged in shared memory
   dev::BTileDev dev() const {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
                          ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
-                         prefetch};
+                         prefetch, poll_depth};
   }
 };
 
@@ -186,6 +190,8 @@ struct bd_inner {
   int* perm = nullptr;        // exact: new -> old
   double* inv = nullptr;      // jacobi
   double* y_int = nullptr;    // forward output (sentinel between solves)
+  double* bt_f = nullptr;     // k_trsv_ptile: forward right-hand side in tile order
+  double* bt_b = nullptr;     // k_trsv_ptile: backward right-hand side in tile order
   double* x_int = nullptr;    // internal backward output for standalone / exact
   HostCsr hlower;
   std::vector<int32_t> hperm;
@@ -807,7 +813,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   // re-lay the schedule out with fixed per-tile strides; external entries as
   // a compact per-tile list (row ranges, input slots, values)
   const int nt = (int)bs.tile_row_ptr.size() - 1;
-  const int ex = bs.Ex, rs = dev::bt_even(bs.tmax), xs = dev::bt_even(bs.xmax);
+  const int ex = bs.Ex, rs = (bs.tmax + 3) & ~3, xs = (bs.xmax + 3) & ~3;  // 16-byte int rows
   const int64_t is = dev::bt_even(rs * (rs + 1) / 2);
   const int rps = dev::bt_round8(rs + 1);
   int emax = 0;
@@ -868,6 +874,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   out->threads = std::max(out->threads, ((xs + 1) / 2 + 31) / 32 * 32);  // <= 2 inputs per thread
   out->sleep_ns = getenv("BD_BTILE_SLEEP") ? atoi(getenv("BD_BTILE_SLEEP")) : 0;
   out->prefetch = getenv("BD_BTILE_PREFETCH") ? atoi(getenv("BD_BTILE_PREFETCH")) : 1;
+  out->poll_depth = getenv("BD_BTILE_POLL") ? atoi(getenv("BD_BTILE_POLL")) : 1;
   out->smem = dev::bt_smem(rs, xs, (int)is, es, rps);
   auto kg = dev::k_trsv_btile<dev::RhsGather>;
   auto kv = dev::k_trsv_btile<dev::RhsVec>;
@@ -883,6 +890,32 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, out->threads, out->smem);
+  {
+    // "reg" (default when tiles fit) | "pipe" | "rsmem" | "smem" (k_trsv_btile)
+    const char* kern = getenv("BD_BTILE_KERNEL");
+    const std::string kn = kern ? kern : "reg";
+    if (kn == "pipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
+      out->pipe = true;
+      out->threads = 256;
+      out->smem = dev::pt_smem(rs, xs, (int)is, es, rps);
+      CK(ctx, cudaFuncSetAttribute(dev::k_trsv_ptile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)out->smem));
+      CK(ctx, cudaFuncSetAttribute(dev::k_trsv_ptile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)out->smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
+    } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
+      out->reg = true;
+      out->reg_smem = kn != "reg";
+      out->threads = 256;
+      out->smem = dev::rt_smem(xs, es, rps, out->reg_smem ? (int)is : 0);
+      if (out->reg_smem)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, dev::k_trsv_rtile<true, dev::RhsSchur>, 256, out->smem);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, dev::k_trsv_rtile<false, dev::RhsSchur>, 256, out->smem);
+    }
+  }
   if (getenv("BD_BTILE_PERSM")) per_sm = std::max(1, std::min(per_sm, atoi(getenv("BD_BTILE_PERSM"))));
   out->grid = (int)std::min<int64_t>(out->ntiles, (int64_t)ctx->nsm * std::max(1, per_sm));
   if (getenv("BD_DEBUG"))
@@ -892,6 +925,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
 }
 
 void free_btile(DevBTile* d) {
+  cudaFree(d->opos);
   cudaFree(d->tile_nr);
   cudaFree(d->task_row);
   cudaFree(d->ent_rp);
@@ -945,6 +979,23 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   if (!ok) return BD_OK;
   TRY(upload_btile(ctx, bl, &p->BL));
   TRY(upload_btile(ctx, bu, &p->BU));
+  if (p->BL.pipe && p->BU.pipe) {
+    // forward rows -> their slot in the backward pass's tile order
+    std::vector<int32_t> pos_u(lower.n, -1), opos((size_t)p->BL.ntiles * p->BL.rs, 0);
+    for (int t = 0; t < p->BU.ntiles; ++t)
+      for (int64_t q = bu.tile_row_ptr[t]; q < bu.tile_row_ptr[t + 1]; ++q)
+        pos_u[bu.task_row[q]] = (int32_t)((int64_t)t * p->BU.rs + (q - bu.tile_row_ptr[t]));
+    for (int t = 0; t < p->BL.ntiles; ++t)
+      for (int64_t q = bl.tile_row_ptr[t]; q < bl.tile_row_ptr[t + 1]; ++q)
+        opos[(size_t)t * p->BL.rs + (q - bl.tile_row_ptr[t])] = pos_u[bl.task_row[q]];
+    CK(ctx, upload_vec(&p->BL.opos, opos));
+    if (dalloc(&p->bt_f, (int64_t)p->BL.ntiles * p->BL.rs) ||
+        dalloc(&p->bt_b, (int64_t)p->BU.ntiles * p->BU.rs))
+      return fail(ctx, BD_ECUDA, "btile: out of device memory");
+    CK(ctx, cudaMemset(p->bt_b, 0, sizeof(double) * (size_t)p->BU.ntiles * p->BU.rs));
+  } else {
+    p->BL.pipe = p->BU.pipe = false;
+  }
   p->btile = true;
   return BD_OK;
 }
@@ -953,8 +1004,15 @@ template <class Rhs>
 bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr_task, int ctr_done, double* reset) {
   bd_ctx* ctx = p->ctx;
-  dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
-                                                                     ctr_done, reset);
+  if (b.reg && b.reg_smem && !reset)
+    dev::k_trsv_rtile<true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
+                                                                             ctr_task, ctr_done);
+  else if (b.reg && !reset)
+    dev::k_trsv_rtile<false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
+                                                                              ctr_task, ctr_done);
+  else
+    dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+                                                                       ctr_done, reset);
   LAUNCHED(ctx);
   return BD_OK;
 }
@@ -1015,6 +1073,24 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->btile && p->BL.pipe) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    const DevBTile& bl = p->BL;
+    const DevBTile& bu = p->BU;
+    dev::k_tile_rhs<Rhs><<<grid_for(ctx, (int64_t)bl.ntiles * bl.rs, dev::TPB), dev::TPB, 0, st>>>(
+        bl.task_row, (int64_t)bl.ntiles * bl.rs, rhs, p->bt_f, p->y_int, p->n, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_ptile<true><<<bl.grid, 256, bl.smem, st>>>(bl.dev(), bl.opos, p->bt_f, p->y_int,
+                                                           p->bt_b, c, ctr0, ctr0 + 1);
+    LAUNCHED(ctx);
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_ptile<false><<<bu.grid, 256, bu.smem, st>>>(bu.dev(), nullptr, p->bt_b, xg, nullptr, c,
+                                                            ctr0 + 2, ctr0 + 3);
+    LAUNCHED(ctx);
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->btile) {
@@ -1807,6 +1883,8 @@ bd_status bd_inner_destroy(bd_inner* p) {
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);
+  cudaFree(p->bt_f);
+  cudaFree(p->bt_b);
   cudaFree(p->x_int);
   ctl_free(&p->ctl);
   delete p;

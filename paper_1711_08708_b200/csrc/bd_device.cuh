@@ -1524,6 +1524,7 @@ struct BTileDev {
   int rs, xs, is, es, rps;          // strides (doubles / elements); 16-byte multiples
   int sleep_ns;                     // cap of the polling back-off (0: spin)
   int prefetch;                     // L2 bulk prefetch of the tile one grid-width ahead
+  int poll_depth;                   // k_trsv_rtile: polls kept in flight per input (1..3)
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
@@ -1711,6 +1712,453 @@ __global__ void __launch_bounds__(256) k_trsv_btile(BTileDev T, Rhs rhs, double*
     c.ctr[ctr_task] = 0u;
     c.ctr[ctr_done] = 0u;
     __threadfence();
+  }
+}
+
+// ---- register-tile triangular solve -------------------------------------------
+// Same schedule and data as k_trsv_btile (tiles of <= 64 rows), but the dense
+// inverse never touches shared memory: during the tile's preparation (before
+// its inputs arrive) each thread loads its 16 entries of inv(L_TT) straight
+// into registers.  Thread mapping: row slot k = 8*warp + lane/4 and column
+// group g = lane%4 (columns g, g+4, ..., g+60), so the 4 partial sums of a row
+// sit in one warp and are combined with two shuffles.  Critical path of a tile
+// after its inputs land: one barrier (inputs -> shared), the external sum
+// (2 entries per lane + 2 shuffles), one barrier (y -> shared), 16 broadcast
+// loads + FMAs, 2 shuffles, publish.  k_trsv_btile had a third barrier and a
+// dense step bound by shared-memory bandwidth (the inverse read from smem).
+constexpr int RT_ROWS = 64;
+
+// Rolling poll: keep three relaxed loads of the word in flight, re-issuing
+// each as soon as it returns the sentinel, so the word is sampled about every
+// third of an L2 round trip instead of once per round trip.
+__device__ __forceinline__ long long poll_rolling3(const double* p) {
+  long long v0, v1, v2;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v0) : "l"(p) : "memory");
+  if (v0 != SENTINEL) return v0;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v1) : "l"(p) : "memory");
+  __nanosleep(100);
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v2) : "l"(p) : "memory");
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v0) : "l"(p) : "memory");
+    if (v1 != SENTINEL) return v1;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v1) : "l"(p) : "memory");
+    if (v2 != SENTINEL) return v2;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v2) : "l"(p) : "memory");
+    if (v0 != SENTINEL) return v0;
+  }
+}
+// shared memory: ys | xin (+zero slot) | ent_val | ent_slot | ent_rp | [inverse (+zero slot)]
+__host__ __device__ constexpr size_t rt_smem(int xs, int es, int rps, int is) {
+  return sizeof(double) * ((size_t)RT_ROWS + xs + 2 + es) + sizeof(unsigned short) * ((size_t)es + rps) +
+         (is > 0 ? sizeof(double) * ((size_t)is + 2) : 0);
+}
+
+// kSmemInv: the inverse is copied to shared memory with cp.async instead of
+// held in registers (fewer registers -> more tiles in flight per SM).
+template <bool kSmemInv, class Rhs>
+__global__ void __launch_bounds__(256, kSmemInv ? 6 : 4) k_trsv_rtile(BTileDev T, Rhs rhs, double* __restrict__ xg,
+                                                       Ctl c, int ctr_task, int ctr_done) {
+  if (inactive(c)) return;
+  extern __shared__ __align__(16) double rt_sm[];
+  double* ys = rt_sm;                 // RT_ROWS
+  double* xin = ys + RT_ROWS;         // xs external inputs, xin[xs] = 0 (zero slot)
+  double* ev = xin + T.xs + 2;        // external entries
+  unsigned short* esl = reinterpret_cast<unsigned short*>(ev + T.es);
+  unsigned short* erp = esl + T.es;
+  double* is_s = reinterpret_cast<double*>(erp + T.rps);  // kSmemInv only
+  __shared__ int task_s;
+  __shared__ int last_s;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int k = warp * 8 + (lane >> 2);  // row slot
+  const int g = lane & 3;                // column group
+  const int jmax = (8 * warp + 7) >> 2;  // warp-uniform: columns g + 4j beyond the warp's rows are zero
+  if (tid == 0) {
+    xin[T.xs] = 0.0;
+    if constexpr (kSmemInv) is_s[T.is] = 0.0;
+  }
+  for (;;) {
+    if (tid == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+    __syncthreads();
+    const int t = task_s;
+    if (t >= T.ntiles) break;
+    unsigned long long* trace = g_tile_trace;
+    if (trace && tid == 0) trace[8 * t] = gtimer();
+    if (tid < (T.prefetch >= 2 ? 5 : T.prefetch) && t + (int)gridDim.x < T.ntiles) {
+      // the tile one grid-width ahead: inverse (prefetch 1); + rows, inputs, entries (2) -> L2
+      const int64_t u = t + (int)gridDim.x;
+      const void* src;
+      unsigned bytes;
+      switch (tid) {
+        case 0: src = T.inv + u * T.is; bytes = T.is * 8; break;
+        case 1: src = T.task_row + u * T.rs; bytes = T.rs * 4; break;
+        case 2: src = T.in_col + u * T.xs; bytes = T.xs * 4; break;
+        case 3: src = T.ent_val + u * T.es; bytes = T.es * 8; break;
+        default: src = T.ent_slot + u * T.es; bytes = T.es * 2; break;
+      }
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(src) + bytes) & ~(uintptr_t)15;
+      if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo))
+                     : "memory");
+    }
+    // preparation: everything up to the polls depends on t only
+    const int nr = T.tile_nr[t];
+    const int row = k < nr ? T.task_row[(int64_t)t * T.rs + k] : -1;
+    int icol[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * nth;
+      icol[h] = j < T.xs ? T.in_col[(int64_t)t * T.xs + j] : -1;
+    }
+    {
+      const double* vb = T.ent_val + (int64_t)t * T.es;
+      for (int q = tid; 2 * q < T.es; q += nth) cp_async16(ev + 2 * q, vb + 2 * q);
+      const unsigned short* sb = T.ent_slot + (int64_t)t * T.es;
+      for (int q = tid; 8 * q < T.es; q += nth) cp_async16(esl + 8 * q, sb + 8 * q);
+      const unsigned short* rb = T.ent_rp + (int64_t)t * T.rps;
+      for (int q = tid; 8 * q < T.rps; q += nth) cp_async16(erp + 8 * q, rb + 8 * q);
+      cp_async_commit();
+    }
+    // inverse entries inv[k][g+4j] (packed column-major: column l = rows l..nr-1
+    // at l*nr - l(l-1)/2); idx(j+1) = idx(j) + 4nr - 4l - 10 with l = g + 4j
+    double a[kSmemInv ? 1 : 16];
+    if constexpr (kSmemInv) {
+      const int ninv = bt_even(nr * (nr + 1) / 2);
+      const double* ib = T.inv + (int64_t)t * T.is;
+      for (int q = tid; 2 * q < ninv; q += nth) cp_async16(is_s + 2 * q, ib + 2 * q);
+      cp_async_commit();
+    } else {
+      const double* ib = T.inv + (int64_t)t * T.is;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int l = g + 4 * j;
+        const bool ok = (j <= jmax) && l <= k && k < nr;
+        const int idx = ok ? l * nr - ((l * (l - 1)) >> 1) + (k - l) : 0;
+        const double v = __ldcs(ib + idx);
+        a[j] = ok ? v : 0.0;
+      }
+    }
+    double b;
+    if constexpr (Rhs::kScalar) {
+      b = rhs.template eval<1>(row, 0);
+    } else {
+      b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
+    }
+    if (trace) {
+      __syncthreads();
+      if (tid == 0) trace[8 * t + 5] = gtimer();
+    }
+    // the tile's distinct inputs: one poller each
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (icol[h] < 0) continue;
+      const double* pj = &xg[icol[h]];
+      long long v;
+      if (T.poll_depth >= 3) {
+        v = poll_rolling3(pj);
+      } else {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+        while (v == SENTINEL) {
+          if (T.sleep_ns) __nanosleep(T.sleep_ns);
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+        }
+      }
+      xin[tid + h * nth] = __longlong_as_double(v);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (trace && tid == 0) trace[8 * t + 4] = gtimer();
+    // y_k = b_k - sum_ext: entries e0+g and e0+g+4 of row k (<= 8 per row),
+    // padding lanes read the zero input slot
+    {
+      const int kc = k < nr ? k : 0;
+      const int e0 = erp[kc], e1 = k < nr ? erp[kc + 1] : e0;
+      double acc = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = e0 + g + 4 * h;
+        const bool ok = e < e1;
+        const int ei = ok ? e : 0;
+        const int sl = ok ? (int)esl[ei] : T.xs;
+        acc = fma(ev[ei], xin[sl], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (g == 0) ys[k] = row >= 0 ? __dsub_rn(b, acc) : 0.0;
+    }
+    if (trace && tid == 0) trace[8 * t + 6] = gtimer();
+    __syncthreads();
+    if (trace && tid == 0) trace[8 * t + 1] = gtimer();
+    // x_k = sum_l inv[k][l] y_l: 4 column groups per row, in-warp combine
+    {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      int idx = g * nr - ((g * (g - 1)) >> 1) + (k - g);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j <= jmax) {
+          double av;
+          if constexpr (kSmemInv) {
+            const int l = g + 4 * j;
+            av = is_s[(l <= k && k < nr) ? idx : T.is];  // branch-free: zero slot
+            idx += 4 * nr - 4 * l - 10;
+          } else {
+            av = a[j];
+          }
+          s[j & 3] = fma(av, ys[g + 4 * j], s[j & 3]);
+        }
+      }
+      double x = (s[0] + s[1]) + (s[2] + s[3]);
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      x += __shfl_xor_sync(0xffffffffu, x, 2);
+      if (g == 0 && row >= 0) publish(&xg[row], x);
+    }
+    if (trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[8 * t + 7] = gtimer();
+      trace[8 * t + 2] = gtimer();
+      trace[8 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && tid == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
+}
+
+// ---- pipelined register-tile triangular solve ---------------------------------
+// k_trsv_rtile with the tile's preparation taken off its critical path: every
+// array a tile needs (inverse, right-hand side in tile order, rows, inputs,
+// external entries) sits at a fixed per-tile stride, so the whole preparation
+// is ONE group of cp.async copies into a shared-memory buffer.  A CTA grabs
+// its next tile as soon as it starts on the current one and streams the next
+// tile's group into the second buffer while it polls and computes (two tiles
+// in flight per CTA; deadlock-free because a CTA finishes its tiles in grab
+// order and the smallest unfinished tile is always being worked on).  The
+// right-hand side is gathered into tile order by k_tile_rhs before the
+// forward pass; the forward pass writes its output both to the polled buffer
+// and, through `opos`, into the backward pass's tile-ordered right-hand side.
+struct PBuf {
+  double* inv;
+  double* b;
+  double* ev;
+  int* row;
+  int* icol;
+  int* opos;
+  unsigned short* esl;
+  unsigned short* erp;
+};
+__host__ __device__ constexpr size_t pt_buf_bytes(int rs, int xs, int is, int es, int rps) {
+  return 8 * ((size_t)is + 2) + 8 * (size_t)rs + 8 * (size_t)es + 4 * (size_t)rs + 4 * (size_t)xs +
+         4 * (size_t)rs + 2 * (size_t)es + 2 * (size_t)rps;
+}
+__host__ __device__ constexpr size_t pt_smem(int rs, int xs, int is, int es, int rps) {
+  return 8 * ((size_t)RT_ROWS + xs + 2) + 2 * pt_buf_bytes(rs, xs, is, es, rps);
+}
+__device__ __forceinline__ PBuf pt_view(char* p, const BTileDev& T) {
+  PBuf B;
+  B.inv = reinterpret_cast<double*>(p);
+  p += 8 * ((size_t)T.is + 2);
+  B.b = reinterpret_cast<double*>(p);
+  p += 8 * (size_t)T.rs;
+  B.ev = reinterpret_cast<double*>(p);
+  p += 8 * (size_t)T.es;
+  B.row = reinterpret_cast<int*>(p);
+  p += 4 * (size_t)T.rs;
+  B.icol = reinterpret_cast<int*>(p);
+  p += 4 * (size_t)T.xs;
+  B.opos = reinterpret_cast<int*>(p);
+  p += 4 * (size_t)T.rs;
+  B.esl = reinterpret_cast<unsigned short*>(p);
+  p += 2 * (size_t)T.es;
+  B.erp = reinterpret_cast<unsigned short*>(p);
+  return B;
+}
+// one commit group: everything tile t needs (strides are 16-byte multiples)
+template <bool kOut>
+__device__ __forceinline__ void pt_issue(const BTileDev& T, const int* __restrict__ opos_g,
+                                         const double* __restrict__ bt, const PBuf& B, int t) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int64_t tt = t;
+  for (int q = tid; 2 * q < T.is; q += nth) cp_async16(B.inv + 2 * q, T.inv + tt * T.is + 2 * q);
+  for (int q = tid; 2 * q < T.rs; q += nth) cp_async16(B.b + 2 * q, bt + tt * T.rs + 2 * q);
+  for (int q = tid; 2 * q < T.es; q += nth) cp_async16(B.ev + 2 * q, T.ent_val + tt * T.es + 2 * q);
+  for (int q = tid; 4 * q < T.rs; q += nth) cp_async16(B.row + 4 * q, T.task_row + tt * T.rs + 4 * q);
+  for (int q = tid; 4 * q < T.xs; q += nth) cp_async16(B.icol + 4 * q, T.in_col + tt * T.xs + 4 * q);
+  if constexpr (kOut)
+    for (int q = tid; 4 * q < T.rs; q += nth) cp_async16(B.opos + 4 * q, opos_g + tt * T.rs + 4 * q);
+  for (int q = tid; 8 * q < T.es; q += nth) cp_async16(B.esl + 8 * q, T.ent_slot + tt * T.es + 8 * q);
+  for (int q = tid; 8 * q < T.rps; q += nth) cp_async16(B.erp + 8 * q, T.ent_rp + tt * T.rps + 8 * q);
+  cp_async_commit();
+}
+
+template <bool kOut>
+__global__ void __launch_bounds__(256, 4) k_trsv_ptile(BTileDev T, const int* __restrict__ opos_g,
+                                                       const double* __restrict__ bt,
+                                                       double* __restrict__ xg,
+                                                       double* __restrict__ bt_next, Ctl c,
+                                                       int ctr_task, int ctr_done) {
+  if (inactive(c)) return;
+  extern __shared__ __align__(16) double pt_sm[];
+  double* ys = pt_sm;          // RT_ROWS
+  double* xin = ys + RT_ROWS;  // xs inputs + zero slot
+  char* bufs = reinterpret_cast<char*>(xin + T.xs + 2);
+  const size_t bufb = pt_buf_bytes(T.rs, T.xs, T.is, T.es, T.rps);
+  __shared__ int task_s;
+  __shared__ int last_s;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int k = warp * 8 + (lane >> 2);
+  const int g = lane & 3;
+  const int jmax = (8 * warp + 7) >> 2;
+  if (tid == 0) {
+    xin[T.xs] = 0.0;
+    reinterpret_cast<double*>(bufs)[T.is] = 0.0;  // zero slots after each inverse
+    reinterpret_cast<double*>(bufs + bufb)[T.is] = 0.0;
+    task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+  }
+  __syncthreads();
+  int t = task_s;
+  int nr = 0;
+  if (t < T.ntiles) {
+    pt_issue<kOut>(T, opos_g, bt, pt_view(bufs, T), t);
+    nr = T.tile_nr[t];
+  }
+  int cur = 0;
+  while (t < T.ntiles) {
+    __syncthreads();  // everyone has read task_s / finished the previous tile
+    if (tid == 0) task_s = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+    __syncthreads();
+    const int tn = task_s;
+    int nr_n = 0;
+    if (tn < T.ntiles) {
+      pt_issue<kOut>(T, opos_g, bt, pt_view(bufs + (cur ^ 1) * bufb, T), tn);
+      nr_n = T.tile_nr[tn];
+    } else {
+      cp_async_commit();  // empty group: keeps wait_group<1> meaning "the current tile"
+    }
+    unsigned long long* trace = g_tile_trace;
+    if (trace && tid == 0) trace[8 * t] = gtimer();
+    cp_async_wait<1>();
+    __syncthreads();
+    const PBuf Bc = pt_view(bufs + cur * bufb, T);
+    if (trace && tid == 0) trace[8 * t + 5] = gtimer();
+    const int row = k < nr ? Bc.row[k] : -1;
+    const int op = kOut && k < nr ? Bc.opos[k] : -1;
+    // inverse entries inv[k][g+4j] into registers (branch-free: zero slot)
+    double a[16];
+    {
+      int idx = g * nr - ((g * (g - 1)) >> 1) + (k - g);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int l = g + 4 * j;
+        a[j] = (j <= jmax) ? Bc.inv[(l <= k && k < nr) ? idx : T.is] : 0.0;
+        idx += 4 * nr - 4 * l - 10;
+      }
+    }
+    // the tile's distinct inputs: one poller each
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * nth;
+      if (j >= T.xs) continue;
+      const int col = Bc.icol[j];
+      if (col < 0) continue;
+      const double* pj = &xg[col];
+      long long v;
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+      while (v == SENTINEL)
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+      xin[j] = __longlong_as_double(v);
+    }
+    __syncthreads();
+    if (trace && tid == 0) trace[8 * t + 4] = gtimer();
+    {
+      const int kc = k < nr ? k : 0;
+      const int e0 = Bc.erp[kc], e1 = k < nr ? Bc.erp[kc + 1] : e0;
+      double acc = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = e0 + g + 4 * h;
+        const bool ok = e < e1;
+        const int ei = ok ? e : 0;
+        const int sl = ok ? (int)Bc.esl[ei] : T.xs;
+        acc = fma(Bc.ev[ei], xin[sl], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (g == 0) ys[k] = row >= 0 ? __dsub_rn(Bc.b[k], acc) : 0.0;
+    }
+    if (trace && tid == 0) trace[8 * t + 6] = gtimer();
+    __syncthreads();
+    if (trace && tid == 0) trace[8 * t + 1] = gtimer();
+    {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j <= jmax) s[j & 3] = fma(a[j], ys[g + 4 * j], s[j & 3]);
+      double x = (s[0] + s[1]) + (s[2] + s[3]);
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      x += __shfl_xor_sync(0xffffffffu, x, 2);
+      if (g == 0 && row >= 0) {
+        publish(&xg[row], x);
+        if constexpr (kOut) bt_next[op] = x;
+      }
+    }
+    if (trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[8 * t + 7] = gtimer();
+      trace[8 * t + 2] = gtimer();
+      trace[8 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
+    }
+    t = tn;
+    nr = nr_n;
+    cur ^= 1;
+  }
+  cp_async_wait<0>();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && tid == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
+}
+
+// Right-hand side of a tile pass gathered into tile order (slot t*rs + k),
+// plus the sentinel fill of the pass's polled output.  Gather right-hand
+// sides (the fused Schur product) use 4 lanes per slot.
+template <class Rhs>
+__global__ void __launch_bounds__(256) k_tile_rhs(const int* __restrict__ task_row, int64_t nslots,
+                                                  Rhs rhs, double* __restrict__ bt,
+                                                  double* __restrict__ fill, int64_t nfill, Ctl c) {
+  if (inactive(c)) return;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < nfill; i += nthr) fill[i] = __longlong_as_double(SENTINEL);
+  if constexpr (Rhs::kScalar) {
+    for (int64_t s = tid; s < nslots; s += nthr) bt[s] = rhs.template eval<1>(task_row[s], 0);
+  } else {
+    // whole warps per iteration (the gather shuffles within groups of 4 lanes)
+    const int64_t nq = (nslots + 7) / 8 * 32;  // lanes needed, rounded to warps
+    for (int64_t q = tid - (threadIdx.x & 31); q < nq; q += nthr) {
+      const int64_t s = (q + (threadIdx.x & 31)) / 4;
+      const int row = s < nslots ? task_row[s] : -1;
+      const double v = rhs.template eval<4>(row, threadIdx.x & 3);
+      if ((threadIdx.x & 3) == 0 && s < nslots) bt[s] = v;
+    }
   }
 }
 

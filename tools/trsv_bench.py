@@ -21,7 +21,10 @@ rng = np.random.default_rng(0)
 y = torch.as_tensor(rng.standard_normal(g.shape[0])).cuda()
 res = {}
 for mode in os.environ.get("MODES", "persist,tiled,syncfree").split(","):
-    os.environ["BD_TRSV"] = mode
+    base, _, kern = mode.partition("@")  # e.g. btile@smem / btile@reg
+    os.environ["BD_TRSV"] = base
+    if kern:
+        os.environ["BD_BTILE_KERNEL"] = kern
     inner = bd.IncompleteCholesky0(); t0 = time.time(); inner.setup(g, coords=wl.mesh.vertices)
     print(mode, "setup", round(time.time()-t0, 2), "s", inner.factor_info(), flush=True)
     z = inner.apply_inverse(y); torch.cuda.synchronize()
