@@ -188,6 +188,20 @@ bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double
                            double dt, double v_rest, double v_span, double tau_open,
                            double tau_close, double u_gate, double* w_new);
 
+/* ---- time-loop bookkeeping (bd/simulate.py:67-89, 190-268) ------------- */
+/* One step's bookkeeping on the device, replacing the host-side passes of
+ * run_simulation over v and u (ActivationTracker.record, bd/simulate.py:74-89;
+ * the depolarisation-band test :229-233; max|u| and weighted_mean_u :240-244):
+ *  phi (device m, NaN = not yet activated) is updated in place: a pending
+ *  vertex with v_new >= threshold gets t_prev + dt*(threshold - v_prev) /
+ *  (v_new - v_prev) if v_prev < threshold, else t_prev (bitwise equal to numpy).
+ * out (HOST double[4]): [0] 1.0 if any v_new lies in [band_lo, band_hi],
+ * [1] 1.0 if every phi is finite after the update, [2] max |u|, [3] the
+ * mass-weighted mean of u (bd/system.py:145).  Synchronises once. */
+bd_status bd_step_track(bd_system* s, const double* v_prev, const double* v_new, double* phi,
+                        double t_prev, double dt, double threshold, double band_lo,
+                        double band_hi, const double* u, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("bd_membrane_rhs_raw", _i32, [_vp, _i64, _i64, _vp, _dbl, _vp, _vp, _vp, C.c_uint64, _dbl,
                                    _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, _vp]),
     ("bd_membrane_gate", _i32, [_vp, _i64, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _vp]),
+    ("bd_step_track", _i32, [_vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, C.POINTER(_dbl)]),
 ]
 
 _lib = None

@@ -214,6 +214,7 @@ struct bd_system {
   int* ell_col = nullptr;
   double* ell_v1 = nullptr;
   double* ell_v2 = nullptr;
+  unsigned long long* track = nullptr;  // bd_step_track flags (lazy)
 };
 
 struct bd_prec {
@@ -1688,6 +1689,7 @@ bd_status bd_system_destroy(bd_system* s) {
   cudaFree(s->ell_col);
   cudaFree(s->ell_v1);
   cudaFree(s->ell_v2);
+  cudaFree(s->track);
   ctl_free(&s->ctl);
   delete s;
   return BD_OK;
@@ -2271,6 +2273,36 @@ bd_status bd_membrane_rhs_raw(bd_ctx* ctx, int64_t n, int64_t m, const double* h
       n, m, v, w, site_mask, active_sites, amplitude, chi, gamma, heart_mass, v_rest, v_span,
       tau_in, tau_out, c_m, rhs, ion);
   LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_step_track(bd_system* s, const double* v_prev, const double* v_new, double* phi,
+                        double t_prev, double dt, double threshold, double band_lo, double band_hi,
+                        const double* u, double* out) {
+  if (!s || !v_prev || !v_new || !phi || !u || !out) return BD_EINVAL;
+  bd_ctx* ctx = s->ctx;
+  Scope sc(ctx);
+  if (!s->track && dalloc(&s->track, 4)) return fail(ctx, BD_ECUDA, "bd_step_track: allocation failed");
+  CK(ctx, cudaMemsetAsync(s->track, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  const int64_t len = std::max(s->n, s->m);
+  dev::k_step_track<<<grid_for(ctx, len, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      s->m, v_prev, v_new, phi, t_prev, dt, threshold, band_lo, band_hi, s->n, u, s->track);
+  LAUNCHED(ctx);
+  TRY(launch_dot(ctx, s->mass, u, s->n, s->ctl, dev::C_WMEAN, dev::FIN_WMEAN, 0, -1, 1));
+  static_assert(sizeof(double) == sizeof(unsigned long long), "");
+  CK(ctx, cudaMemcpyAsync(ctx->h_pin, s->track, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->h_pin + 3, s->ctl.sc + dev::S_WMEAN, sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long bits[3];
+  std::memcpy(bits, ctx->h_pin, sizeof(bits));
+  out[0] = bits[0] ? 1.0 : 0.0;
+  out[1] = bits[1] ? 0.0 : 1.0;  // covered = no unset vertex left
+  double umax;
+  std::memcpy(&umax, &bits[2], sizeof(double));
+  out[2] = umax;
+  out[3] = ctx->h_pin[3];
   return BD_OK;
 }
 

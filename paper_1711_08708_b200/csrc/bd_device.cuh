@@ -2789,5 +2789,54 @@ __global__ void k_membrane_gate(int64_t m, const double* __restrict__ v, const d
   }
 }
 
+// Time-loop bookkeeping of one step (bd/simulate.py:67-89, 229-245): the
+// running first-crossing activation map with sub-step interpolation, the
+// depolarisation-band / full-coverage flags and max|u|.  flags[0] |= any
+// v_new in [lo, hi]; flags[1] |= any phi still unset after the update;
+// flags[2] = max over |u| as ordered bits (non-negative doubles order like
+// their bit patterns, so the integer max is exact and deterministic).
+__global__ void __launch_bounds__(TPB) k_step_track(int64_t m, const double* __restrict__ v_prev,
+                                                    const double* __restrict__ v_new,
+                                                    double* __restrict__ phi, double t_prev,
+                                                    double dt, double thr, double lo, double hi,
+                                                    int64_t n, const double* __restrict__ u,
+                                                    unsigned long long* __restrict__ flags) {
+  int band = 0, unset = 0;
+  unsigned long long umax = 0ull;
+  const int64_t len = m > n ? m : n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < len;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (k < m) {
+      const double vn = v_new[k];
+      double ph = phi[k];
+      if (!isfinite(ph) && vn >= thr) {
+        const double vp = v_prev[k];
+        // frac = (thr - v_prev) / (v_new - v_prev); phi = t_prev + dt * frac
+        ph = vp < thr ? __dadd_rn(t_prev, __dmul_rn(dt, __ddiv_rn(__dsub_rn(thr, vp), __dsub_rn(vn, vp))))
+                      : t_prev;
+        phi[k] = ph;
+      }
+      band |= (vn >= lo) && (vn <= hi);
+      unset |= !isfinite(ph);
+    }
+    if (k < n) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(u[k]));
+      umax = b > umax ? b : umax;
+    }
+  }
+  band = __syncthreads_or(band);
+  unset = __syncthreads_or(unset);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long q = __shfl_xor_sync(0xffffffffu, umax, o);
+    umax = q > umax ? q : umax;
+  }
+  if (threadIdx.x == 0) {
+    if (band) atomicOr(&flags[0], 1ull);
+    if (unset) atomicOr(&flags[1], 1ull);
+  }
+  if ((threadIdx.x & 31) == 0 && umax) atomicMax(&flags[2], umax);
+}
+
 }  // namespace dev
 }  // namespace bd

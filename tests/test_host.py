@@ -201,3 +201,19 @@ def test_lattice_tiles_depth():
     dr = int(re.search(r"tile-DAG depth (\d+)", out_rcb).group(1))
     assert dg == 81, out_grid
     assert dr > 2 * dg, out_rcb
+
+
+# ---- host activation tracker (reference tests/test_simulate.py:25-52) -------------
+def test_activation_times_kats(rng):
+    from paper_1711_08708_b200.simulate import ActivationTracker, activation_times
+
+    np.testing.assert_array_equal(activation_times(np.full((3, 2), 50.0), dt=1.0).phi, [0.0, 0.0])
+    assert activation_times(np.array([[-90.0], [-30.0], [-10.0]]), dt=1.0).phi[0] == 1.5
+    never = activation_times(np.full((5, 3), -90.0), dt=0.5)
+    assert not np.isfinite(never.phi).any() and not never.all_activated()
+    history = np.cumsum(rng.uniform(-5, 15, size=(20, 6)), axis=0) - 90.0
+    batch = activation_times(history, 0.25)
+    tr = ActivationTracker(6, history[0])
+    for k in range(1, 20):
+        tr.record(history[k - 1], history[k], (k - 1) * 0.25, 0.25)
+    np.testing.assert_array_equal(tr.result().phi, batch.phi)
