@@ -112,12 +112,14 @@ def build_workload(name, inner, cells=None):
     return wl
 
 
-def assemble(wl):
+def assemble(wl, mode=None):
     from paper_1711_08708_b200.precond import build_monodomain_matrix
     from paper_1711_08708_b200.system import BidomainSystem
+    mode = mode or os.environ.get("BD_ASSEMBLY", "device")  # P1 assembly on the GPU (setup)
     t0 = time.perf_counter()
-    sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
-    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+    sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False,
+                                assembly=mode)
+    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers, assembly=mode)
     return sysm, km, time.perf_counter() - t0
 
 
@@ -442,7 +444,7 @@ def run_reference(args, rank):
     from oracle import bidomain_oracle as orc
     from paper_1711_08708_b200.ionic import stimulus_vector
     wl = build_workload(args.workload, args.inner)
-    sysm, km, t_asm = assemble(wl)
+    sysm, km, t_asm = assemble(wl, "host")  # the reference's own (numpy) assembly
     pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, wl.inner)
     n, m = sysm.n, sysm.n_heart
     fx = os.path.join(REPO, "tests", "golden", f"{wl.name}_{wl.inner}_oracle.json")

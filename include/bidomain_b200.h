@@ -188,6 +188,26 @@ bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double
                            double dt, double v_rest, double v_span, double tau_open,
                            double tau_close, double u_gate, double* w_new);
 
+/* ---- P1 assembly on the device (setup; bd/assembly.py:36-97) ---------- */
+/* Stiffness K = sum_e vol_e * sym(G_e sigma_e G_e^T) and the row-sum lumped
+ * mass m_v = sum_e vol_e/(dim+1), assembled on the device.  Host inputs:
+ * vertices (nv x dim, fp64 row-major; the space's vertices are 0..nv-1),
+ * elements (ne x (dim+1) int64), sigma (ne x dim x dim).  If sigma2 is given
+ * the element tensor is the harmonic mean sym(inv(inv(sigma)+inv(sigma2)))
+ * (the monodomain tensor of build_monodomain_matrix, bd/precond.py:34-47).
+ * Result: sorted CSR with duplicates summed in element order (deterministic),
+ * explicit zeros kept like the reference's COO -> CSR.  BD_EINVAL on a
+ * non-positive element volume (AssemblyError in the reference). */
+typedef struct bd_asm bd_asm;
+bd_status bd_assemble_p1(bd_ctx* ctx, int dim, int64_t nv, const double* vertices, int64_t ne,
+                         const int64_t* elements, const double* sigma, const double* sigma2,
+                         bd_asm** out, int64_t* nnz);
+/* Copy the result to host arrays (indptr nv+1, indices nnz, data nnz,
+ * mass nv); any pointer may be NULL. */
+bd_status bd_assemble_export(bd_asm* a, int64_t* indptr, int32_t* indices, double* data,
+                             double* mass);
+bd_status bd_assemble_destroy(bd_asm* a);
+
 /* ---- time-loop bookkeeping (bd/simulate.py:67-89, 190-268) ------------- */
 /* One step's bookkeeping on the device, replacing the host-side passes of
  * run_simulation over v and u (ActivationTracker.record, bd/simulate.py:74-89;

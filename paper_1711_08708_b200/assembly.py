@@ -6,6 +6,13 @@ with duplicates summed and indices sorted; row-sum-lumped mass.  Elements are
 processed in chunks so the 6.3M-tet (config 2) and 50M-tet (config 3) meshes
 assemble in bounded memory; meshes below one chunk reproduce the reference's
 arrays exactly.
+
+`DeviceAssembler` is the same discretisation on the GPU (`bd_assemble_p1`,
+csrc/bd_assembly.cuh): the element tensors are formed once
+on the host, local matrices / gradients / harmonic means and the
+COO -> CSR reduction (stable radix sort, sequential per-entry sums in element
+order) run on the device.  Entries agree with the host path to rounding
+(different summation order); the lumped mass is summed in the reference order.
 """
 from __future__ import annotations
 
@@ -90,3 +97,100 @@ def lumped_mass_diagonal(mesh: Mesh, space: Space = Space.FULL) -> np.ndarray:
 
 def assemble_lumped_mass(mesh: Mesh, space: Space = Space.FULL) -> sp.csr_matrix:
     return sp.csr_matrix(sp.diags(lumped_mass_diagonal(mesh, space)))
+
+
+class DeviceAssembler:
+    """All blocks of one (mesh, params, fibres) on the GPU: S_1 (bar1), S_i
+    (intra, heart), S_e (bar_e), K_m stiffness (harmonic mean, heart) and the
+    two lumped masses.  Heart tensors are evaluated once on the host."""
+
+    def __init__(self, mesh: Mesh, field_params, fibers=None):
+        from . import _lib
+
+        self._lib = _lib
+        self.ctx = _lib.Context.default()
+        self.mesh = mesh
+        d = mesh.dim
+        self.heart = mesh.tags == Region.HEART
+        self.verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        self.el = np.ascontiguousarray(mesh.elements, dtype=np.int64)
+        self.el_h = np.ascontiguousarray(self.el[self.heart])
+        tf = TensorField(field_params, d, "bar1", fibers)
+        cent = self.verts[self.el_h].mean(axis=1)
+        self.intra, self.extra = (np.ascontiguousarray(a, dtype=np.float64)
+                                  for a in tf._heart_tensors(cent))
+        self.params = field_params
+        self._mass = {}
+
+    def _torso(self, base: np.ndarray) -> np.ndarray:
+        """Full-element tensor array: heart rows from `base`, torso c·I."""
+        d = self.mesh.dim
+        out = np.zeros((self.el.shape[0], d, d))
+        out[self.heart] = base
+        known = self.heart.copy()
+        for t in (Region.TORSO_LUNG, Region.TORSO_CAVITY, Region.TORSO_OTHER):
+            mask = self.mesh.tags == t
+            if mask.any():
+                out[mask] = self.params.torso_conductivity(t) * np.eye(d)
+            known |= mask
+        if not known.all():
+            raise ValueError("unknown region tag in mesh")
+        return out
+
+    def _run(self, el, nv, sigma, sigma2=None, space=Space.FULL):
+        L = self._lib
+        C = __import__("ctypes")
+        h = C.c_void_p()
+        nnz = C.c_int64()
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        s2 = None if sigma2 is None else np.ascontiguousarray(sigma2, dtype=np.float64)
+        st = L.lib().bd_assemble_p1(self.ctx.handle, self.mesh.dim, int(nv), self.verts.ctypes.data,
+                                    int(el.shape[0]), el.ctypes.data, sigma.ctypes.data,
+                                    None if s2 is None else s2.ctypes.data, C.byref(h),
+                                    C.byref(nnz))
+        if st == L.BD_EINVAL:
+            raise AssemblyError(L.lib().bd_last_error(self.ctx.handle).decode())
+        L.check(st, self.ctx.handle)
+        try:
+            n = int(nnz.value)
+            indptr = np.empty(nv + 1, dtype=np.int64)
+            indices = np.empty(n, dtype=np.int32)
+            data = np.empty(n, dtype=np.float64)
+            mass = np.empty(nv, dtype=np.float64)
+            L.check(L.lib().bd_assemble_export(h, indptr.ctypes.data, indices.ctypes.data,
+                                               data.ctypes.data, mass.ctypes.data),
+                    self.ctx.handle)
+        finally:
+            L.lib().bd_assemble_destroy(h)
+        self._mass.setdefault(space, mass)
+        return sp.csr_matrix((data, indices, indptr), shape=(nv, nv)), mass
+
+    def stiffness(self, kind: str) -> sp.csr_matrix:
+        n, m = self.mesh.vertex_count, self.mesh.heart_vertex_count
+        if kind == "bar1":
+            return self._run(self.el, n, self._torso(self.intra + self.extra))[0]
+        if kind == "bar_e":
+            return self._run(self.el, n, self._torso(self.extra))[0]
+        if kind == "intra":
+            return self._run(self.el_h, m, self.intra, space=Space.HEART_ONLY)[0]
+        if kind == "mono":
+            return self._run(self.el_h, m, self.intra, self.extra, space=Space.HEART_ONLY)[0]
+        raise ValueError(f"unknown tensor field kind {kind!r}")
+
+    def lumped_mass(self, space: Space = Space.FULL) -> np.ndarray:
+        if space not in self._mass:
+            self.stiffness("bar1" if space == Space.FULL else "intra")
+        return self._mass[space]
+
+
+_DEV_CACHE: dict = {}
+
+
+def device_assembler(mesh: Mesh, params, fibers=None) -> DeviceAssembler:
+    """One cached DeviceAssembler per (mesh, params, fibres) (the system and
+    the monodomain matrix share the heart tensors)."""
+    key = (id(mesh), id(params), id(fibers))
+    a = _DEV_CACHE.get("last")
+    if a is None or a[0] != key:
+        _DEV_CACHE["last"] = (key, DeviceAssembler(mesh, params, fibers))
+    return _DEV_CACHE["last"][1]

@@ -16,6 +16,9 @@
 #include <vector>
 
 #include "../../include/bidomain_b200.h"
+#include "bd_assembly.cuh"
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include "bd_device.cuh"
 #include "bd_host.hpp"
 
@@ -2303,6 +2306,150 @@ bd_status bd_step_track(bd_system* s, const double* v_prev, const double* v_new,
   std::memcpy(&umax, &bits[2], sizeof(double));
   out[2] = umax;
   out[3] = ctx->h_pin[3];
+  return BD_OK;
+}
+
+// ---- P1 assembly on the device (setup) -------------------------------------------
+struct bd_asm {
+  bd_ctx* ctx;
+  int64_t nv = 0, nnz = 0;
+  long long* rowptr = nullptr;
+  int* col = nullptr;
+  double* data = nullptr;
+  double* mass = nullptr;
+};
+
+bd_status bd_assemble_destroy(bd_asm* a) {
+  if (!a) return BD_OK;
+  cudaFree(a->rowptr);
+  cudaFree(a->col);
+  cudaFree(a->data);
+  cudaFree(a->mass);
+  delete a;
+  return BD_OK;
+}
+
+bd_status bd_assemble_p1(bd_ctx* ctx, int dim, int64_t nv, const double* vertices, int64_t ne,
+                         const int64_t* elements, const double* sigma, const double* sigma2,
+                         bd_asm** out, int64_t* nnz_out) {
+  if (!ctx || !out || !vertices || (ne > 0 && (!elements || !sigma)) || nv <= 0 ||
+      (dim != 2 && dim != 3))
+    return fail(ctx, BD_EINVAL, "bd_assemble_p1: bad arguments");
+  Scope sc(ctx);
+  cudaStream_t st = ctx->stream;
+  const int A = dim + 1;
+  const int64_t np = ne * A * A;
+  bd_asm* a = new bd_asm;
+  a->ctx = ctx;
+  a->nv = nv;
+  asmk::DevScratch S;  // scratch, freed at scope exit
+  auto bail = [&](const std::string& msg) {
+    bd_assemble_destroy(a);
+    return fail(ctx, BD_ECUDA, msg);
+  };
+  double *xv, *sa, *sb = nullptr, *local, *vol;
+  int64_t* el;
+  int* bad;
+  unsigned long long *k0, *k1, *v0, *v1, *ukey;
+  long long *head, *pos, *start;
+  if (S.get(&xv, nv * dim) || S.get(&el, ne * A) || S.get(&sa, ne * dim * dim) ||
+      (sigma2 && S.get(&sb, ne * dim * dim)) || S.get(&local, np) || S.get(&vol, ne) ||
+      S.get(&bad, 1) || S.get(&k0, np) || S.get(&k1, np) || S.get(&v0, np) || S.get(&v1, np))
+    return bail("bd_assemble_p1: device allocation failed");
+  CK(ctx, cudaMemcpyAsync(xv, vertices, sizeof(double) * nv * dim, cudaMemcpyHostToDevice, st));
+  if (ne > 0) {
+    CK(ctx, cudaMemcpyAsync(el, elements, sizeof(int64_t) * ne * A, cudaMemcpyHostToDevice, st));
+    CK(ctx, cudaMemcpyAsync(sa, sigma, sizeof(double) * ne * dim * dim, cudaMemcpyHostToDevice, st));
+    if (sigma2)
+      CK(ctx, cudaMemcpyAsync(sb, sigma2, sizeof(double) * ne * dim * dim, cudaMemcpyHostToDevice, st));
+  }
+  CK(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const int gl = grid_for(ctx, std::max<int64_t>(ne, 1), 256);
+  const int gp = grid_for(ctx, std::max<int64_t>(np, 1), 256);
+  if (ne > 0) {
+    if (dim == 2) {
+      asmk::k_local<2><<<gl, 256, 0, st>>>(ne, xv, el, sa, sb, local, vol, bad);
+      asmk::k_keys<2><<<gp, 256, 0, st>>>(ne, el, nv, k0, v0);
+    } else {
+      asmk::k_local<3><<<gl, 256, 0, st>>>(ne, xv, el, sa, sb, local, vol, bad);
+      asmk::k_keys<3><<<gp, 256, 0, st>>>(ne, el, nv, k0, v0);
+    }
+    LAUNCHED(ctx);
+  }
+  int hbad = 0;
+  CK(ctx, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(ctx, cudaStreamSynchronize(st));
+  if (hbad) {
+    bd_assemble_destroy(a);
+    return fail(ctx, BD_EINVAL, "degenerate element (non-positive volume)");
+  }
+  int end_bit = 1;
+  while (end_bit < 64 && (((unsigned long long)nv * (unsigned long long)nv - 1ull) >> end_bit)) ++end_bit;
+  // stable LSD radix sort: equal keys keep element order
+  size_t tmp_bytes = 0;
+  cub::DoubleBuffer<unsigned long long> dk(k0, k1), dv(v0, v1);
+  CK(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, np, 0, end_bit, st));
+  void* tmp = nullptr;
+  if (S.get((char**)&tmp, (int64_t)tmp_bytes)) return bail("bd_assemble_p1: sort scratch");
+  if (np > 0) CK(ctx, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, dv, np, 0, end_bit, st));
+  const unsigned long long* keys = dk.Current();
+  const unsigned long long* vals = dv.Current();
+  if (S.get(&head, np) || S.get(&pos, np)) return bail("bd_assemble_p1: allocation failed");
+  int64_t nnz = 0;
+  if (np > 0) {
+    asmk::k_heads<<<gp, 256, 0, st>>>(np, keys, head);
+    LAUNCHED(ctx);
+    size_t sb_bytes = 0;
+    CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, sb_bytes, head, pos, np, st));
+    void* tmp2 = nullptr;
+    if (S.get((char**)&tmp2, (int64_t)sb_bytes)) return bail("bd_assemble_p1: scan scratch");
+    CK(ctx, cub::DeviceScan::ExclusiveSum(tmp2, sb_bytes, head, pos, np, st));
+    long long last[2];
+    CK(ctx, cudaMemcpyAsync(&last[0], pos + np - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(&last[1], head + np - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    nnz = last[0] + last[1];
+  }
+  if (S.get(&start, nnz) || S.get(&ukey, nnz) || dalloc(&a->col, std::max<int64_t>(nnz, 1)) ||
+      dalloc(&a->data, std::max<int64_t>(nnz, 1)) || dalloc(&a->mass, nv) ||
+      dalloc(&a->rowptr, nv + 1))
+    return bail("bd_assemble_p1: allocation failed");
+  CK(ctx, cudaMemsetAsync(a->mass, 0, sizeof(double) * nv, st));
+  if (nnz > 0) {
+    asmk::k_seg_start<<<gp, 256, 0, st>>>(np, head, pos, start);
+    const int gu = grid_for(ctx, nnz, 256);
+    if (dim == 2)
+      asmk::k_segsum<2><<<gu, 256, 0, st>>>(nnz, np, nv, start, keys, vals, local, vol, a->col,
+                                            a->data, ukey, a->mass);
+    else
+      asmk::k_segsum<3><<<gu, 256, 0, st>>>(nnz, np, nv, start, keys, vals, local, vol, a->col,
+                                            a->data, ukey, a->mass);
+    LAUNCHED(ctx);
+  }
+  asmk::k_rowptr<<<grid_for(ctx, nv + 1, 256), 256, 0, st>>>(nv, nnz, ukey, a->rowptr);
+  LAUNCHED(ctx);
+  CK(ctx, cudaStreamSynchronize(st));
+  a->nnz = nnz;
+  *nnz_out = nnz;
+  *out = a;
+  return BD_OK;
+}
+
+bd_status bd_assemble_export(bd_asm* a, int64_t* indptr, int32_t* indices, double* data,
+                             double* mass) {
+  if (!a) return BD_EINVAL;
+  bd_ctx* ctx = a->ctx;
+  Scope sc(ctx);
+  cudaStream_t st = ctx->stream;
+  static_assert(sizeof(long long) == sizeof(int64_t), "");
+  if (indptr)
+    CK(ctx, cudaMemcpyAsync(indptr, a->rowptr, sizeof(int64_t) * (a->nv + 1), cudaMemcpyDeviceToHost, st));
+  if (indices && a->nnz)
+    CK(ctx, cudaMemcpyAsync(indices, a->col, sizeof(int32_t) * a->nnz, cudaMemcpyDeviceToHost, st));
+  if (data && a->nnz)
+    CK(ctx, cudaMemcpyAsync(data, a->data, sizeof(double) * a->nnz, cudaMemcpyDeviceToHost, st));
+  if (mass) CK(ctx, cudaMemcpyAsync(mass, a->mass, sizeof(double) * a->nv, cudaMemcpyDeviceToHost, st));
+  CK(ctx, cudaStreamSynchronize(st));
   return BD_OK;
 }
 

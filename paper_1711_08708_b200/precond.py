@@ -29,13 +29,21 @@ INNER_NAMES = ("exact", "ic0", "jacobi")
 
 
 def build_monodomain_matrix(mesh: Mesh, params: ConductivityParams, gamma: float,
-                            fibers=None) -> sp.csr_matrix:
-    """K_m = S(harmonic-mean tensor) + γ diag(M_H) (bd/precond.py:34-47)."""
+                            fibers=None, assembly: str = "host") -> sp.csr_matrix:
+    """K_m = S(harmonic-mean tensor) + γ diag(M_H) (bd/precond.py:34-47);
+    assembly="device" assembles the stiffness on the GPU."""
     if gamma <= 0:
         raise ValueError("gamma must be strictly positive")
-    stiff = assemble_stiffness(mesh, TensorField(params, mesh.dim, "mono", fibers),
-                               Space.HEART_ONLY)
-    mass = lumped_mass_diagonal(mesh, Space.HEART_ONLY)
+    if assembly == "device":
+        from .assembly import device_assembler
+        da = device_assembler(mesh, params, fibers)
+        stiff, mass = da.stiffness("mono"), da.lumped_mass(Space.HEART_ONLY)
+    elif assembly == "host":
+        stiff = assemble_stiffness(mesh, TensorField(params, mesh.dim, "mono", fibers),
+                                   Space.HEART_ONLY)
+        mass = lumped_mass_diagonal(mesh, Space.HEART_ONLY)
+    else:
+        raise ValueError(f"unknown assembly mode {assembly!r}")
     out = (stiff + gamma * sp.diags(mass)).tocsr()
     out.sum_duplicates()
     out.sort_indices()

@@ -137,9 +137,21 @@ class BidomainSystem:
 
     @classmethod
     def build(cls, mesh: Mesh, params: ConductivityParams, dt: float, fibers=None,
-              with_extra: bool = True) -> "BidomainSystem":
-        """Assemble all blocks for time step dt (bd/system.py:82-97)."""
+              with_extra: bool = True, assembly: str = "host") -> "BidomainSystem":
+        """Assemble all blocks for time step dt (bd/system.py:82-97).
+        assembly="device" runs the P1 assembly on the GPU (DeviceAssembler)."""
         d = mesh.dim
+        if assembly == "device":
+            from .assembly import device_assembler
+            da = device_assembler(mesh, params, fibers)
+            return cls(stiff_total=da.stiffness("bar1"), stiff_intra=da.stiffness("intra"),
+                       stiff_extra=da.stiffness("bar_e") if with_extra else None,
+                       mass_diag=da.lumped_mass(Space.FULL),
+                       heart_mass_diag=da.lumped_mass(Space.HEART_ONLY),
+                       gamma=gamma(params.chi, params.c_m, dt), mesh=mesh, params=params,
+                       fibers=fibers)
+        if assembly != "host":
+            raise ValueError(f"unknown assembly mode {assembly!r}")
         return cls(
             stiff_total=assemble_stiffness(mesh, TensorField(params, d, "bar1", fibers)),
             stiff_intra=assemble_stiffness(mesh, TensorField(params, d, "intra", fibers),
