@@ -151,6 +151,7 @@ struct DevBTile {
   bool pipe = false;      // k_trsv_ptile (pipelined; needs opos / tile-ordered rhs)
   int* opos = nullptr;    // forward schedule: slot of each row in the backward tile order
   bool reg = false;       // k_trsv_rtile instead of k_trsv_btile
+  bool tile_rhs = false;  // k_trsv_rtile with the right-hand side pre-gathered in tile order
   bool reg_smem = false;  // k_trsv_rtile with the inverse staged in shared memory
   dev::BTileDev dev() const {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
@@ -895,7 +896,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, out->threads, out->smem);
   {
-    // "reg" (default when tiles fit) | "pipe" | "rsmem" | "smem" (k_trsv_btile)
+    // "reg" (default when tiles fit) | "regt" | "pipe" | "rsmem" | "smem" (k_trsv_btile)
     const char* kern = getenv("BD_BTILE_KERNEL");
     const std::string kn = kern ? kern : "reg";
     if (kn == "pipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
@@ -909,15 +910,16 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
     } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
       out->reg = true;
-      out->reg_smem = kn != "reg";
+      out->reg_smem = kn == "rsmem";
+      out->tile_rhs = kn == "regt";
       out->threads = 256;
       out->smem = dev::rt_smem(xs, es, rps, out->reg_smem ? (int)is : 0);
       if (out->reg_smem)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, dev::k_trsv_rtile<true, dev::RhsSchur>, 256, out->smem);
+            &per_sm, dev::k_trsv_rtile<true, false, dev::RhsSchur>, 256, out->smem);
       else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, dev::k_trsv_rtile<false, dev::RhsSchur>, 256, out->smem);
+            &per_sm, dev::k_trsv_rtile<false, false, dev::RhsSchur>, 256, out->smem);
     }
   }
   if (getenv("BD_BTILE_PERSM")) per_sm = std::max(1, std::min(per_sm, atoi(getenv("BD_BTILE_PERSM"))));
@@ -983,7 +985,7 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   if (!ok) return BD_OK;
   TRY(upload_btile(ctx, bl, &p->BL));
   TRY(upload_btile(ctx, bu, &p->BU));
-  if (p->BL.pipe && p->BU.pipe) {
+  if ((p->BL.pipe && p->BU.pipe) || (p->BL.tile_rhs && p->BU.tile_rhs)) {
     // forward rows -> their slot in the backward pass's tile order
     std::vector<int32_t> pos_u(lower.n, -1), opos((size_t)p->BL.ntiles * p->BL.rs, 0);
     for (int t = 0; t < p->BU.ntiles; ++t)
@@ -999,6 +1001,7 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
     CK(ctx, cudaMemset(p->bt_b, 0, sizeof(double) * (size_t)p->BU.ntiles * p->BU.rs));
   } else {
     p->BL.pipe = p->BU.pipe = false;
+    p->BL.tile_rhs = p->BU.tile_rhs = false;
   }
   p->btile = true;
   return BD_OK;
@@ -1009,11 +1012,11 @@ bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* x
                        int ctr_task, int ctr_done, double* reset) {
   bd_ctx* ctx = p->ctx;
   if (b.reg && b.reg_smem && !reset)
-    dev::k_trsv_rtile<true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
-                                                                             ctr_task, ctr_done);
+    dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr);
   else if (b.reg && !reset)
-    dev::k_trsv_rtile<false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c,
-                                                                              ctr_task, ctr_done);
+    dev::k_trsv_rtile<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr);
   else
     dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
                                                                        ctr_done, reset);
@@ -1077,6 +1080,24 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_jacobi<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, p->inv, rhs, out ? out : x_int, c,
                                                       ctr0, fin, slot, slot2, nmean);
     LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (p->btile && p->BL.tile_rhs) {
+    double* xg = (out && !p->perm) ? out : x_int;
+    const DevBTile& bl = p->BL;
+    const DevBTile& bu = p->BU;
+    dev::k_tile_rhs<Rhs><<<grid_for(ctx, (int64_t)bl.ntiles * bl.rs, dev::TPB), dev::TPB, 0, st>>>(
+        bl.task_row, (int64_t)bl.ntiles * bl.rs, rhs, p->bt_f, p->y_int, p->n, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_rtile<false, true, Rhs><<<bl.grid, 256, bl.smem, st>>>(
+        bl.dev(), rhs, p->y_int, c, ctr0, ctr0 + 1, p->bt_f, bl.opos, p->bt_b);
+    LAUNCHED(ctx);
+    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    LAUNCHED(ctx);
+    dev::k_trsv_rtile<false, true, dev::RhsGather><<<bu.grid, 256, bu.smem, st>>>(
+        bu.dev(), dev::RhsGather{nullptr}, xg, c, ctr0 + 2, ctr0 + 3, p->bt_b, nullptr, nullptr);
+    LAUNCHED(ctx);
+    if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     return BD_OK;
   }
   if (p->btile && p->BL.pipe) {

@@ -1755,9 +1755,15 @@ __host__ __device__ constexpr size_t rt_smem(int xs, int es, int rps, int is) {
 
 // kSmemInv: the inverse is copied to shared memory with cp.async instead of
 // held in registers (fewer registers -> more tiles in flight per SM).
-template <bool kSmemInv, class Rhs>
-__global__ void __launch_bounds__(256, kSmemInv ? 6 : 4) k_trsv_rtile(BTileDev T, Rhs rhs, double* __restrict__ xg,
-                                                       Ctl c, int ctr_task, int ctr_done) {
+// kTileRhs: the right-hand side comes pre-gathered in tile order (bt, slot
+// t*rs + k, see k_tile_rhs) instead of through the Rhs functor, so the tile's
+// preparation is a single round of independent loads; with bt_next set the
+// pass also writes its output into the next pass's tile order through opos.
+template <bool kSmemInv, bool kTileRhs, class Rhs>
+__global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
+    k_trsv_rtile(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
+                 const double* __restrict__ bt, const int* __restrict__ opos,
+                 double* __restrict__ bt_next) {
   if (inactive(c)) return;
   extern __shared__ __align__(16) double rt_sm[];
   double* ys = rt_sm;                 // RT_ROWS
@@ -1840,7 +1846,11 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4) k_trsv_rtile(BTileDev T
       }
     }
     double b;
-    if constexpr (Rhs::kScalar) {
+    int op = -1;
+    if constexpr (kTileRhs) {
+      b = bt[(int64_t)t * T.rs + k];  // k < rs: padding slots hold 0
+      if (bt_next && k < nr) op = opos[(int64_t)t * T.rs + k];
+    } else if constexpr (Rhs::kScalar) {
       b = rhs.template eval<1>(row, 0);
     } else {
       b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
@@ -1911,7 +1921,10 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4) k_trsv_rtile(BTileDev T
       double x = (s[0] + s[1]) + (s[2] + s[3]);
       x += __shfl_xor_sync(0xffffffffu, x, 1);
       x += __shfl_xor_sync(0xffffffffu, x, 2);
-      if (g == 0 && row >= 0) publish(&xg[row], x);
+      if (g == 0 && row >= 0) {
+        publish(&xg[row], x);
+        if (kTileRhs && op >= 0) bt_next[op] = x;
+      }
     }
     if (trace && tid == 0) {
       unsigned smid;
