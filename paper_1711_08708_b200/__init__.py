@@ -25,4 +25,7 @@ from .krylov import SolveStats, dump_residuals, pcg_solve
 from .simulate import (ActivationMap, SimState, SimulationResult, SimulationSetup,
                        activation_times, run_simulation, time_step)
 
+from .vtkio import read_mesh_vtk, write_activation_csv, write_fields_vtk, write_mesh_vtk
+from . import study, vtkio  # bd/bench.py study harness, bd/vtkio.py formats
+
 __version__ = "0.1.0"
