@@ -936,37 +936,66 @@ bool build_btile_schedule(const DTileSchedule& ds, BTileSchedule* out, std::stri
     out->tile_in_ptr.push_back((int32_t)out->in_col.size());
     out->xmax = std::max<int>(out->xmax, (int)loc.size());
   }
-  std::vector<long double> x;
+  // packed sizes first (each block padded to an even length), then the
+  // independent per-tile inverses in parallel (host threads)
+  out->tile_inv_ptr.assign(ntiles + 1, 0);
   for (int t = 0; t < ntiles; ++t) {
-    const int r0 = ds.tile_row_ptr[t], nr = ds.tile_row_ptr[t + 1] - r0;
-    // X = A^{-1} for the tile block A (lower triangular in slot order):
-    // X[k][l] = (delta_kl - sum_{l<=j<k} A[k][j] X[j][l]) / A[k][k]
-    x.assign((size_t)nr * nr, 0.0L);
-    for (int k = 0; k < nr; ++k) {
-      const int64_t q = r0 + k;
-      const long double d = ds.task_diag[q];
-      if (!(d != 0.0L)) {
-        *why = "zero pivot in a tile block";
-        return false;
-      }
-      for (int e = 0; e < E; ++e) {
-        const int32_t code = ds.ell_col[q * E + e];
-        if (code >= 0 || code == zero) continue;
-        const int j = -code - 1;
-        if (j >= k) {
-          *why = "tile block is not triangular in slot order";
-          return false;
+    const int64_t nr = ds.tile_row_ptr[t + 1] - ds.tile_row_ptr[t];
+    const int64_t len = nr * (nr + 1) / 2;
+    out->tile_inv_ptr[t + 1] = out->tile_inv_ptr[t] + len + (len & 1);
+  }
+  out->inv.assign(out->tile_inv_ptr[ntiles], 0.0);
+  int failed = 0;
+  std::string fail_why;
+#pragma omp parallel
+  {
+    std::vector<long double> x;
+#pragma omp for schedule(dynamic, 16)
+    for (int t = 0; t < ntiles; ++t) {
+      if (failed) continue;
+      const int r0 = ds.tile_row_ptr[t], nr = ds.tile_row_ptr[t + 1] - r0;
+      // X = A^{-1} for the tile block A (lower triangular in slot order):
+      // X[k][l] = (delta_kl - sum_{l<=j<k} A[k][j] X[j][l]) / A[k][k]
+      x.assign((size_t)nr * nr, 0.0L);
+      const char* err = nullptr;
+      for (int k = 0; k < nr && !err; ++k) {
+        const int64_t q = r0 + k;
+        const long double d = ds.task_diag[q];
+        if (!(d != 0.0L)) {
+          err = "zero pivot in a tile block";
+          break;
         }
-        const long double a = ds.ell_val[q * E + e];
-        for (int l = 0; l <= j; ++l) x[(size_t)k * nr + l] -= a * x[(size_t)j * nr + l];
+        for (int e = 0; e < E; ++e) {
+          const int32_t code = ds.ell_col[q * E + e];
+          if (code >= 0 || code == zero) continue;
+          const int j = -code - 1;
+          if (j >= k) {
+            err = "tile block is not triangular in slot order";
+            break;
+          }
+          const long double a = ds.ell_val[q * E + e];
+          for (int l = 0; l <= j; ++l) x[(size_t)k * nr + l] -= a * x[(size_t)j * nr + l];
+        }
+        if (err) break;
+        x[(size_t)k * nr + k] += 1.0L;
+        for (int l = 0; l <= k; ++l) x[(size_t)k * nr + l] /= d;
       }
-      x[(size_t)k * nr + k] += 1.0L;
-      for (int l = 0; l <= k; ++l) x[(size_t)k * nr + l] /= d;
+      if (err) {
+#pragma omp critical
+        {
+          failed = 1;
+          fail_why = err;
+        }
+        continue;
+      }
+      double* dst = out->inv.data() + out->tile_inv_ptr[t];
+      for (int k = 0; k < nr; ++k)
+        for (int l = 0; l <= k; ++l) *dst++ = (double)x[(size_t)k * nr + l];
     }
-    for (int k = 0; k < nr; ++k)
-      for (int l = 0; l <= k; ++l) out->inv.push_back((double)x[(size_t)k * nr + l]);
-    if (out->inv.size() & 1) out->inv.push_back(0.0);
-    out->tile_inv_ptr.push_back((int64_t)out->inv.size());
+  }
+  if (failed) {
+    *why = fail_why;
+    return false;
   }
   return true;
 }
