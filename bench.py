@@ -123,6 +123,17 @@ def assemble(wl, mode=None):
     return sysm, km, time.perf_counter() - t0
 
 
+def trsv_kernel():
+    """Name of the triangular-solve kernel the library runs (BD_TRSV /
+    BD_BTILE_KERNEL knobs, defaults btile + reg -> k_trsv_rtile)."""
+    mode = os.environ.get("BD_TRSV", "btile")
+    if mode != "btile":
+        return f"trsv_{mode}"
+    kern = os.environ.get("BD_BTILE_KERNEL", "reg")
+    return {"reg": "trsv_rtile", "regt": "trsv_rtile", "rsmem": "trsv_rtile",
+            "pipe": "trsv_ptile"}.get(kern, "trsv_btile")
+
+
 def tri_bytes(nnz, rows):
     """Algorithmic bytes of one triangular pass."""
     return 12 * nnz + 4 * (rows + 1) + 16 * rows
@@ -263,8 +274,7 @@ def run_native(args, rank, world, local_rank):
     ncu_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(ncu_path):
         with open(ncu_path) as fh:
-            traffic = json.load(fh).get(
-                f"{wl.name}_{wl.inner}_{os.environ.get('BD_TRSV', 'btile')}_bulk_solve_bytes")
+            traffic = json.load(fh).get(f"{wl.name}_{wl.inner}_{trsv_kernel()}_bulk_solve_bytes")
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -289,7 +299,7 @@ def run_native(args, rank, world, local_rank):
                     "wall_s": round(wall_e2e, 3)},
             "roofline": {"bound": "hbm",
                          "kernel": ("bulk inner solve pair: forward + backward triangular pass "
-                                    f"(k_trsv_{os.environ.get('BD_TRSV', 'btile')}, P_1 block)")
+                                    f"(k_{trsv_kernel()}, P_1 block)")
                                    if wl.inner != "jacobi" else "jacobi",
                          "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",

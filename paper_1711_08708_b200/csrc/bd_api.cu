@@ -147,6 +147,9 @@ struct DevBTile {
   double* inv = nullptr;
   int ntiles = 0, rs = 0, xs = 0, is = 0, es = 0, rps = 0, grid = 0, threads = 256, sleep_ns = 0,
       prefetch = 1, poll_depth = 3;
+  double* inbox = nullptr;  // shared per inner (not owned here)
+  int* dst = nullptr;
+  int dmax = 0;
   size_t smem = 0;
   bool pipe = false;      // k_trsv_ptile (pipelined; needs opos / tile-ordered rhs)
   int* opos = nullptr;    // forward schedule: slot of each row in the backward tile order
@@ -156,7 +159,7 @@ struct DevBTile {
   dev::BTileDev dev() const {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
                          ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
-                         prefetch, poll_depth};
+                         prefetch, poll_depth, inbox,    dst,      dmax};
   }
 };
 
@@ -196,6 +199,8 @@ struct bd_inner {
   double* y_int = nullptr;    // forward output (sentinel between solves)
   double* bt_f = nullptr;     // k_trsv_ptile: forward right-hand side in tile order
   double* bt_b = nullptr;     // k_trsv_ptile: backward right-hand side in tile order
+  double* inbox = nullptr;    // k_trsv_rtile inbox mode: per-tile input slots (sentinel between passes)
+  int64_t inbox_len = 0;
   double* x_int = nullptr;    // internal backward output for standalone / exact
   HostCsr hlower;
   std::vector<int32_t> hperm;
@@ -931,6 +936,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
 }
 
 void free_btile(DevBTile* d) {
+  cudaFree(d->dst);
   cudaFree(d->opos);
   cudaFree(d->tile_nr);
   cudaFree(d->task_row);
@@ -985,6 +991,44 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   if (!ok) return BD_OK;
   TRY(upload_btile(ctx, bl, &p->BL));
   TRY(upload_btile(ctx, bu, &p->BU));
+  // inbox mode (BD_BTILE_INBOX=1; measured 1.5% slower than polling the output
+  // vector): per pass, the inbox slots (consumer tile, input slot)
+  // fed by each row
+  const char* ib = getenv("BD_BTILE_INBOX");
+  if (p->BL.reg && p->BU.reg && !p->BL.tile_rhs && !p->BL.reg_smem && ib && atoi(ib) == 1) {
+    bool ok = true;
+    for (int pass = 0; pass < 2 && ok; ++pass) {
+      const BTileSchedule& bs = pass ? bu : bl;
+      DevBTile& db = pass ? p->BU : p->BL;
+      std::vector<std::vector<int32_t>> need(lower.n);
+      const int nt = db.ntiles;
+      for (int c = 0; c < nt; ++c)
+        for (int32_t j = 0; j < bs.tile_in_ptr[c + 1] - bs.tile_in_ptr[c]; ++j)
+          need[bs.in_col[bs.tile_in_ptr[c] + j]].push_back((int32_t)((int64_t)c * db.xs + j));
+      int dmax = 1;
+      for (const auto& v : need) dmax = std::max<int>(dmax, (int)v.size());
+      if (dmax > 8 || (int64_t)nt * db.xs >= INT32_MAX) {
+        ok = false;
+        break;
+      }
+      std::vector<int32_t> dst((size_t)nt * db.rs * dmax, -1);
+      for (int t = 0; t < nt; ++t)
+        for (int64_t q = bs.tile_row_ptr[t]; q < bs.tile_row_ptr[t + 1]; ++q) {
+          const auto& v = need[bs.task_row[q]];
+          const size_t base = ((size_t)t * db.rs + (size_t)(q - bs.tile_row_ptr[t])) * dmax;
+          for (size_t d = 0; d < v.size(); ++d) dst[base + d] = v[d];
+        }
+      CK(ctx, upload_vec(&db.dst, dst));
+      db.dmax = dmax;
+      p->inbox_len = std::max<int64_t>(p->inbox_len, (int64_t)nt * db.xs);
+    }
+    if (ok) {
+      if (dalloc(&p->inbox, p->inbox_len)) return fail(ctx, BD_ECUDA, "btile: inbox allocation");
+      p->BL.inbox = p->BU.inbox = p->inbox;
+    } else {
+      p->BL.dmax = p->BU.dmax = 0;
+    }
+  }
   if ((p->BL.pipe && p->BU.pipe) || (p->BL.tile_rhs && p->BU.tile_rhs)) {
     // forward rows -> their slot in the backward pass's tile order
     std::vector<int32_t> pos_u(lower.n, -1), opos((size_t)p->BL.ntiles * p->BL.rs, 0);
@@ -1123,10 +1167,16 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     // sentinel fills right before each pass: besides resetting the polled
     // buffers they leave them L2-resident, so polls and publishes hit L2
     // (folding the resets into the passes measured ~30% slower passes)
-    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
+    // (inbox mode: only the inboxes are polled, so only they are reset)
+    const bool ib = p->BL.inbox != nullptr;
+    const int64_t nf1 = ib ? (int64_t)p->BL.ntiles * p->BL.xs : p->n;
+    const int64_t nf2 = ib ? (int64_t)p->BU.ntiles * p->BU.xs : p->n;
+    dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
+                                                                  dev::SENTINEL, c);
     LAUNCHED(ctx);
     TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr));
-    dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(xg, p->n, dev::SENTINEL, c);
+    dev::k_fill<<<grid_for(ctx, nf2, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : xg, nf2,
+                                                                  dev::SENTINEL, c);
     LAUNCHED(ctx);
     TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr));
     if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
@@ -1911,6 +1961,7 @@ bd_status bd_inner_destroy(bd_inner* p) {
   cudaFree(p->y_int);
   cudaFree(p->bt_f);
   cudaFree(p->bt_b);
+  cudaFree(p->inbox);
   cudaFree(p->x_int);
   ctl_free(&p->ctl);
   delete p;

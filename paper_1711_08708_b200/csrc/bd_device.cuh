@@ -1525,6 +1525,12 @@ struct BTileDev {
   int sleep_ns;                     // cap of the polling back-off (0: spin)
   int prefetch;                     // L2 bulk prefetch of the tile one grid-width ahead
   int poll_depth;                   // k_trsv_rtile: polls kept in flight per input (1..3)
+  // inbox mode (k_trsv_rtile): producers push each value into the input slots
+  // of its consumer tiles (inbox[c*xs + j]); a tile polls its own contiguous
+  // inbox instead of scattered rows of the output vector
+  double* inbox;                    // nullptr: poll the output vector
+  const int* dst;                   // [tile][rs][dmax] inbox slots fed by each row (-1 pad)
+  int dmax;                         // <= 8
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
@@ -1845,6 +1851,12 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
         a[j] = ok ? v : 0.0;
       }
     }
+    int dsl[2] = {-1, -1};  // inbox slots this lane feeds (lanes g: entries 2g, 2g+1)
+    if (T.inbox && k < nr) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (2 * g + h < T.dmax) dsl[h] = T.dst[((int64_t)t * T.rs + k) * T.dmax + 2 * g + h];
+    }
     double b;
     int op = -1;
     if constexpr (kTileRhs) {
@@ -1863,7 +1875,7 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (icol[h] < 0) continue;
-      const double* pj = &xg[icol[h]];
+      const double* pj = T.inbox ? &T.inbox[(int64_t)t * T.xs + tid + h * nth] : &xg[icol[h]];
       long long v;
       if (T.poll_depth >= 3) {
         v = poll_rolling3(pj);
@@ -1921,7 +1933,16 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
       double x = (s[0] + s[1]) + (s[2] + s[3]);
       x += __shfl_xor_sync(0xffffffffu, x, 1);
       x += __shfl_xor_sync(0xffffffffu, x, 2);
-      if (g == 0 && row >= 0) {
+      if (T.inbox) {
+        // push into the consumers' inboxes first (critical), then the output
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (dsl[h] >= 0) publish(&T.inbox[dsl[h]], x);
+        if (g == 0 && row >= 0) {
+          xg[row] = x;
+          if (kTileRhs && op >= 0) bt_next[op] = x;
+        }
+      } else if (g == 0 && row >= 0) {
         publish(&xg[row], x);
         if (kTileRhs && op >= 0) bt_next[op] = x;
       }

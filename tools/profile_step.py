@@ -14,8 +14,9 @@ ap.add_argument("--workload", default="cfg2")
 ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
 wl = configs.BUILDERS[a.workload]()
-sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
-km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False,
+                               assembly="device")
+km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers, assembly="device")
 pre = bd.BlockLUPreconditioner(sysm, inner=wl.inner, monodomain_matrix=km)
 state = bd.SimState.resting(sysm.n, sysm.n_heart, wl.ionic)
 pts = wl.mesh.vertices[: sysm.n_heart]
