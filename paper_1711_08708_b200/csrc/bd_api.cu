@@ -150,6 +150,7 @@ struct DevBTile {
   double* inbox = nullptr;  // shared per inner (not owned here)
   int* dst = nullptr;
   int dmax = 0;
+  int exw = 8;  // max external entries per row
   size_t smem = 0;
   bool pipe = false;      // k_trsv_ptile (pipelined; needs opos / tile-ordered rhs)
   int* opos = nullptr;    // forward schedule: slot of each row in the backward tile order
@@ -159,7 +160,7 @@ struct DevBTile {
   dev::BTileDev dev() const {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
                          ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
-                         prefetch, poll_depth, inbox,    dst,      dmax};
+                         prefetch, poll_depth, inbox,    dst,      dmax,     exw};
   }
 };
 
@@ -781,8 +782,31 @@ bd_status setup_dtile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   const bool grid = !(part && std::string(part) == "rcb");
   int ntiles = (int)std::max<int64_t>(1, lower.n / target);
   std::vector<int32_t> tile;
+  // Row orderings that concatenate coordinate-sorted blocks (the heart-first
+  // numbering of bd/mesh.py:252-263: heart vertices, then torso vertices, each
+  // in lattice order) make lattice tiles that mix the blocks cyclic.  Detect
+  // the blocks as the descents of the lexicographic coordinate order and keep
+  // them in separate tiles (partition_grid's class argument).
+  std::vector<int32_t> cls;
+  if (coords && dim > 0) {
+    int nd = 0;
+    cls.assign(lower.n, 0);
+    for (int64_t i = 1; i < lower.n; ++i) {
+      bool less = false;  // coords[i] < coords[i-1] lexicographically
+      for (int a = 0; a < dim; ++a) {
+        const double x = coords[i * dim + a], y = coords[(i - 1) * dim + a];
+        if (x != y) {
+          less = x < y;
+          break;
+        }
+      }
+      nd += less;
+      cls[i] = nd;
+    }
+    if (nd == 0 || nd > 8) cls.clear();
+  }
   if (coords && dim > 0 && grid)
-    ntiles = partition_grid(lower.n, dim, coords, target, nullptr, &tile);
+    ntiles = partition_grid(lower.n, dim, coords, target, cls.empty() ? nullptr : &cls, &tile);
   else if (coords && dim > 0)
     partition_coords(lower.n, dim, coords, ntiles, &tile);
   else
@@ -834,6 +858,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
     emax = std::max(emax, cnt);
   }
   const int es = dev::bt_round8(std::max(emax, 1));
+  out->exw = ex;
   if (emax > 65535 || bs.xmax > 65535) return fail(ctx, BD_EINVAL, "btile: tile too large");
   std::vector<int32_t> nr(nt), row((size_t)nt * rs, -1), in((size_t)nt * xs, -1);
   std::vector<uint16_t> rp((size_t)nt * rps, 0), slot((size_t)nt * es, 0);
@@ -903,7 +928,8 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   {
     // "reg" (default when tiles fit) | "regt" | "pipe" | "rsmem" | "smem" (k_trsv_btile)
     const char* kern = getenv("BD_BTILE_KERNEL");
-    const std::string kn = kern ? kern : "reg";
+    std::string kn = kern ? kern : "reg";
+    if (ex > 8 && kn != "pipe") kn = "reg";  // k_trsv_btile / rsmem / regt handle <= 8 entries per row
     if (kn == "pipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
       out->pipe = true;
       out->threads = 256;
@@ -913,7 +939,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       CK(ctx, cudaFuncSetAttribute(dev::k_trsv_ptile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)out->smem));
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
-    } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
+    } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && (ex <= 8 || kn == "reg") && ex <= 16) {
       out->reg = true;
       out->reg_smem = kn == "rsmem";
       out->tile_rhs = kn == "regt";
@@ -955,8 +981,31 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   const bool grid = !(part && std::string(part) == "rcb");
   int ntiles = (int)std::max<int64_t>(1, lower.n / target);
   std::vector<int32_t> tile;
+  // Row orderings that concatenate coordinate-sorted blocks (the heart-first
+  // numbering of bd/mesh.py:252-263: heart vertices, then torso vertices, each
+  // in lattice order) make lattice tiles that mix the blocks cyclic.  Detect
+  // the blocks as the descents of the lexicographic coordinate order and keep
+  // them in separate tiles (partition_grid's class argument).
+  std::vector<int32_t> cls;
+  if (coords && dim > 0) {
+    int nd = 0;
+    cls.assign(lower.n, 0);
+    for (int64_t i = 1; i < lower.n; ++i) {
+      bool less = false;  // coords[i] < coords[i-1] lexicographically
+      for (int a = 0; a < dim; ++a) {
+        const double x = coords[i * dim + a], y = coords[(i - 1) * dim + a];
+        if (x != y) {
+          less = x < y;
+          break;
+        }
+      }
+      nd += less;
+      cls[i] = nd;
+    }
+    if (nd == 0 || nd > 8) cls.clear();
+  }
   if (coords && dim > 0 && grid)
-    ntiles = partition_grid(lower.n, dim, coords, target, nullptr, &tile);
+    ntiles = partition_grid(lower.n, dim, coords, target, cls.empty() ? nullptr : &cls, &tile);
   else if (coords && dim > 0)
     partition_coords(lower.n, dim, coords, ntiles, &tile);
   else
@@ -978,7 +1027,8 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
          build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
   }
   ok = ok && build_btile_schedule(dl, &bl, &why) && build_btile_schedule(du, &bu, &why);
-  if (ok && (std::max(bl.tmax, bu.tmax) > 256 || std::max(bl.Ex, bu.Ex) > 8 ||
+  if (ok && (std::max(bl.tmax, bu.tmax) > 256 || std::max(bl.Ex, bu.Ex) > 16 ||
+             (std::max(bl.Ex, bu.Ex) > 8 && std::max(bl.tmax, bu.tmax) > dev::RT_ROWS) ||
              std::max(bl.xmax, bu.xmax) > 512 ||
              std::max(bl.tmax, bu.tmax) > (int)std::sqrt(2.0 * 24000))) {
     ok = false;

@@ -1531,6 +1531,7 @@ struct BTileDev {
   double* inbox;                    // nullptr: poll the output vector
   const int* dst;                   // [tile][rs][dmax] inbox slots fed by each row (-1 pad)
   int dmax;                         // <= 8
+  int exw;                          // max external entries of a row (k_trsv_rtile: <= 16)
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
@@ -1898,7 +1899,8 @@ __global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
       const int e0 = erp[kc], e1 = k < nr ? erp[kc + 1] : e0;
       double acc = 0.0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < 4; ++h) {
+        if (h >= 2 && 4 * h >= T.exw) break;  // rows with > 8 entries: heart-first torso rows
         const int e = e0 + g + 4 * h;
         const bool ok = e < e1;
         const int ei = ok ? e : 0;

@@ -1,0 +1,76 @@
+"""GPU, BASELINE config 4 at the first point of its mesh-size sweep (96^3 box,
+912,673 vertices, 26,578 heart vertices; ellipsoidal ventricle in a 20 cm
+torso, helical fibres, apex stimulus, ic0, tol 1e-10) against the CPU oracle
+run recorded by `tools/oracle_fullsize.py --config cfg4 --cells 96`
+(tests/golden/cfg4_96_ic0_oracle.json):
+
+* identical inputs (host assembly, bit-identical to the reference): per-step
+  iterations within ±2, probe traces within 1e-6, state rel-L2 (strided
+  subsample) within 1e-8 — the BASELINE parity targets (measured: 2e-16..2e-13);
+* the P1 blocks assembled on the device: same iteration / trace bounds, state
+  within 1e-7.  The device sums element contributions in a different order, so
+  entries that the reference rounds to exactly 0.0 (and drops from the IC(0)
+  pattern) survive as rounding residues; the preconditioner then differs in a
+  few pattern entries and the two solves agree to the PCG tolerance level
+  (measured 1.4e-8) instead of to rounding."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FIX = os.path.join(GOLDEN, "cfg4_96_ic0_oracle.json")
+
+
+@pytest.fixture(scope="module", params=["host", "device"])
+def run(request):
+    import paper_1711_08708_b200 as bd
+    from paper_1711_08708_b200 import configs
+    from paper_1711_08708_b200.precond import build_monodomain_matrix
+    if not os.path.exists(FIX):
+        pytest.skip("cfg4 96^3 oracle fixture not recorded")
+    ref = json.load(open(FIX))
+    wl = configs.cfg4(96)
+    mode = request.param
+    sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False,
+                                   assembly=mode)
+    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers, assembly=mode)
+    # same operator: sizes and entry checksums (the device keeps explicit zeros
+    # that the chunked host sum drops, so nnz may only grow)
+    assert sysm.n == ref["n"] and sysm.n_heart == ref["m"]
+    assert sysm.stiff_total.nnz >= ref["nnz_S1"] and km.nnz >= ref["nnz_Km"]
+    assert abs(np.abs(sysm.stiff_total.data).sum() / ref["checksum_S1"] - 1) <= 1e-12
+    assert abs(np.abs(km.data).sum() / ref["checksum_Km"] - 1) <= 1e-12
+    pre = bd.BlockLUPreconditioner(sysm, inner="ic0", monodomain_matrix=km)
+    state = bd.SimState.resting(sysm.n, sysm.n_heart, wl.ionic)
+    pts = wl.mesh.vertices[: sysm.n_heart]
+    out = {"iters": [], "trace": [], "u": [], "v": []}
+    for _ in range(len(ref["iters"])):
+        state, st = bd.time_step(state, sysm, pre, wl.ionic, wl.protocol, wl.dt, tol=wl.tol,
+                                 max_iter=20000, heart_points=pts)
+        out["iters"].append(st.iterations)
+        v = state.v.cpu().numpy()
+        out["trace"].append(v[wl.probes])
+        out["u"].append(state.u.cpu().numpy())
+        out["v"].append(v)
+    return ref, out, mode
+
+
+def test_cfg4_iterations_traces_state(run):
+    ref, out, mode = run
+    k = len(out["iters"])
+    assert np.max(np.abs(np.array(out["iters"]) - np.array(ref["iters"][:k]))) <= 2
+    tr, rt = np.array(out["trace"]), np.array(ref["trace"][:k])
+    assert np.max(np.abs(tr - rt) / np.maximum(np.abs(rt), 1.0)) <= 1e-6
+    s = ref["sub_stride"]
+    for j in range(min(len(ref["u_sub"]), k)):
+        ru, rv = np.array(ref["u_sub"][j]), np.array(ref["v_sub"][j])
+        gu, gv = out["u"][j][::s], out["v"][j][::s]
+        rel = np.sqrt(np.sum((gu - ru) ** 2) + np.sum((gv - rv) ** 2)) / np.sqrt(
+            np.sum(ru ** 2) + np.sum(rv ** 2))
+        print(f"{mode} assembly, step {j + 1}: rel-L2 {rel:.3e}")
+        assert rel <= (1e-8 if mode == "host" else 1e-7), (j, rel)

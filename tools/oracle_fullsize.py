@@ -31,9 +31,10 @@ def main():
     ap.add_argument("--steps", type=int, default=13)
     ap.add_argument("--inner", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--cells", type=int, default=None, help="mesh size (cfg0/1/4 builders)")
     a = ap.parse_args()
     t0 = time.perf_counter()
-    wl = configs.BUILDERS[a.config]()
+    wl = configs.BUILDERS[a.config](a.cells) if a.cells else configs.BUILDERS[a.config]()
     inner = a.inner or wl.inner
     sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
     km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
@@ -41,8 +42,9 @@ def main():
     t0 = time.perf_counter()
     pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, inner)
     t_setup = time.perf_counter() - t0
-    out_path = a.out or os.path.join(REPO, "tests", "golden", f"{a.config}_{inner}_oracle.json")
-    rec = {"config": a.config, "inner": inner, "n": sysm.n, "m": sysm.n_heart,
+    tag = f"{a.config}_{a.cells}" if a.cells else a.config
+    out_path = a.out or os.path.join(REPO, "tests", "golden", f"{tag}_{inner}_oracle.json")
+    rec = {"config": a.config, "cells": a.cells, "inner": inner, "n": sysm.n, "m": sysm.n_heart,
            "nnz_S1": int(sysm.stiff_total.nnz), "nnz_Si": int(sysm.stiff_intra.nnz),
            "nnz_Km": int(km.nnz), "assembly_s": t_asm, "setup_s": t_setup,
            "checksum_S1": float(np.abs(sysm.stiff_total.data).sum()),
