@@ -36,9 +36,8 @@ def _same(dev, host):
     scale = np.repeat(np.maximum(abs(host).max(axis=1).toarray().ravel(), 1e-300),
                       np.diff(host.indptr))
     assert (np.abs(dev.data - host.data) <= 1e-13 * scale).all()
-    # every entry the host stores as nonzero is nonzero on the device too (the
-    # device may keep rounding-level residues where the host's sum is exactly 0.0)
-    assert not np.any((host.data != 0.0) & (dev.data == 0.0))
+    # (which entries round to exactly 0.0 depends on the summation order, so
+    # the two may differ there; tests/test_gpu_fullsize_cfg4.py bounds the effect)
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
