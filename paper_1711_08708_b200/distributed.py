@@ -24,6 +24,7 @@ collectives are torch.distributed (NCCL over NVLink on the box).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -379,7 +380,7 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
         rho.copy_(torch.where(act, rho_next, rho))
         active.copy_(act)
 
-    use_graph = graph if graph is not None else (dev.type == "cuda")
+    use_graph = graph if graph is not None else (dev.type == "cuda" and os.environ.get("BD_SHARDED_GRAPH", "1") != "0")
     g = None
     k_done = 0
     if use_graph:
