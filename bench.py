@@ -129,8 +129,8 @@ def trsv_kernel():
     mode = os.environ.get("BD_TRSV", "btile")
     if mode != "btile":
         return f"trsv_{mode}"
-    kern = os.environ.get("BD_BTILE_KERNEL", "reg")
-    return {"reg": "trsv_rtile", "regt": "trsv_rtile", "rsmem": "trsv_rtile",
+    kern = os.environ.get("BD_BTILE_KERNEL", "auto")
+    return {"auto": "trsv_rtile", "reg": "trsv_rtile", "regt": "trsv_rtile", "rsmem": "trsv_rtile",
             "pipe": "trsv_ptile"}.get(kern, "trsv_btile")
 
 

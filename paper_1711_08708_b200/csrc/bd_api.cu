@@ -926,10 +926,36 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, out->threads, out->smem);
   {
-    // "reg" (default when tiles fit) | "regt" | "pipe" | "rsmem" | "smem" (k_trsv_btile)
+    // "auto" (default) | "reg" | "rsmem" | "regt" | "pipe" | "smem" (k_trsv_btile)
     const char* kern = getenv("BD_BTILE_KERNEL");
-    std::string kn = kern ? kern : "reg";
-    if (ex > 8 && kn != "pipe") kn = "reg";  // k_trsv_btile / rsmem / regt handle <= 8 entries per row
+    std::string kn = kern ? kern : "auto";
+    if (kn == "auto") {
+      // Latency-bound passes (few tiles per level of the tile DAG) want the
+      // register inverse (shortest on-path compute); throughput-bound ones
+      // (wide levels, e.g. config 3) want more tiles in flight per SM, i.e.
+      // the inverse staged in shared memory (6 CTAs/SM instead of 4).
+      // Measured crossover: cfg2 ~230 tiles/level -> reg,
+      // 192x192x96 ~470 and cfg3 ~900 -> rsmem.
+      std::vector<int32_t> row_tile(bs.task_row.empty() ? 0 : 1 + *std::max_element(
+                                                                    bs.task_row.begin(), bs.task_row.end()), -1);
+      for (int t = 0; t < nt; ++t)
+        for (int64_t q = bs.tile_row_ptr[t]; q < bs.tile_row_ptr[t + 1]; ++q) row_tile[bs.task_row[q]] = t;
+      std::vector<int32_t> lev(nt, 0);
+      int depth = 0;
+      for (int t = 0; t < nt; ++t) {  // task order is topological
+        int l = 0;
+        for (int32_t j = bs.tile_in_ptr[t]; j < bs.tile_in_ptr[t + 1]; ++j)
+          l = std::max(l, lev[row_tile[bs.in_col[j]]] + 1);
+        lev[t] = l;
+        depth = std::max(depth, l + 1);
+      }
+      const double width = (double)nt / std::max(1, depth);
+      kn = width > 350.0 ? "rsmem" : "reg";
+      if (getenv("BD_DEBUG"))
+        std::fprintf(stderr, "[bd] btile auto: %d tiles, tile-DAG depth %d, %.0f tiles/level -> %s\n", nt,
+                     depth, width, kn.c_str());
+    }
+    if (ex > 8 && kn == "smem") kn = "reg";  // k_trsv_btile handles <= 8 external entries per row
     if (kn == "pipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 8) {
       out->pipe = true;
       out->threads = 256;
@@ -939,7 +965,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       CK(ctx, cudaFuncSetAttribute(dev::k_trsv_ptile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)out->smem));
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
-    } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && (ex <= 8 || kn == "reg") && ex <= 16) {
+    } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) {
       out->reg = true;
       out->reg_smem = kn == "rsmem";
       out->tile_rhs = kn == "regt";

@@ -14,7 +14,8 @@ cells = tuple(int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "128,128,64
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 wl = configs.cfg2(cells)
 t0 = time.time()
-S1 = assemble_stiffness(wl.mesh, TensorField(wl.params, 3, "bar1", wl.fibers))
+from paper_1711_08708_b200.assembly import DeviceAssembler
+S1 = DeviceAssembler(wl.mesh, wl.params, wl.fibers).stiffness("bar1")
 g = regularize_stiffness(S1).grounded()
 print(f"n={g.shape[0]} nnz={g.nnz} assembly {time.time()-t0:.1f}s", flush=True)
 rng = np.random.default_rng(0)
