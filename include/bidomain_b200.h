@@ -81,6 +81,13 @@ bd_status bd_csr_create(bd_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
 bd_status bd_csr_destroy(bd_csr* a);
 /* y = alpha*A*x + beta*y (device pointers). */
 bd_status bd_spmv(bd_csr* a, const double* x, double* y, double alpha, double beta);
+/* y = alpha * A [x ; x_ghost] + beta * y with the input split in two device
+ * arrays: column c < nsplit reads x[c], column c >= nsplit reads
+ * x_ghost[c - nsplit] (a sharded rank's owned entries and its halo, without
+ * concatenating them).  Needs the ELL copy bd_csr_create builds for short,
+ * near-uniform rows (P1 stencils); BD_EINVAL otherwise. */
+bd_status bd_spmv_split(bd_csr* a, const double* x, int64_t nsplit, const double* x_ghost,
+                        double* y, double alpha, double beta);
 
 /* ---- vector primitives (BlockVector.dot/norm, bd/system.py:39-43) ------ */
 /* Deterministic fixed-order dot product; synchronising (result on host). */

@@ -50,6 +50,7 @@ SIGNATURES = [
     ("bd_csr_create", _i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _pp]),
     ("bd_csr_destroy", _i32, [_vp]),
     ("bd_spmv", _i32, [_vp, _vp, _vp, _dbl, _dbl]),
+    ("bd_spmv_split", _i32, [_vp, _vp, _i64, _vp, _vp, _dbl, _dbl]),
     ("bd_dot", _i32, [_vp, _i64, _vp, _vp, C.POINTER(_dbl)]),
     ("bd_mean", _i32, [_vp, _i64, _vp, C.POINTER(_dbl)]),
     ("bd_system_create", _i32, [_vp, _vp, _vp, _vp, _vp, _dbl, _pp]),

@@ -53,6 +53,10 @@ struct bd_csr {
   int* col = nullptr;
   double* val = nullptr;
   int G = 8;
+  // entry-major ELL copy for bd_spmv when rows are short and near-uniform
+  int ell_w = 0;
+  int* ell_col = nullptr;
+  double* ell_val = nullptr;
   dev::Csr dev() const { return dev::Csr{(int)nrows, rowptr, col, val}; }
 };
 
@@ -1713,12 +1717,35 @@ bd_status bd_csr_create(bd_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz,
     bd_csr_destroy(a);
     return fail(ctx, BD_ECUDA, "bd_csr_create: device allocation/copy failed");
   }
+  {  // ELL copy (P1 stencils: <= 32 entries per row, little padding)
+    int64_t maxlen = 0;
+    for (int64_t i = 0; i < nrows; ++i) maxlen = std::max<int64_t>(maxlen, indptr[i + 1] - indptr[i]);
+    const int W = maxlen <= 8 ? 8 : maxlen <= 16 ? 16 : maxlen <= 24 ? 24 : maxlen <= 32 ? 32 : 0;
+    if (W && nnz > 0 && (double)W * nrows <= 1.5 * (double)nnz && !getenv("BD_NO_SPMV_ELL")) {
+      std::vector<int> ec((size_t)W * nrows, -1);
+      std::vector<double> ev((size_t)W * nrows, 0.0);
+      for (int64_t i = 0; i < nrows; ++i)
+        for (int64_t q = indptr[i]; q < indptr[i + 1]; ++q) {
+          ec[(size_t)(q - indptr[i]) * nrows + i] = indices[q];
+          ev[(size_t)(q - indptr[i]) * nrows + i] = values[q];
+        }
+      if (dalloc(&a->ell_col, (int64_t)W * nrows) || dalloc(&a->ell_val, (int64_t)W * nrows) ||
+          cudaMemcpy(a->ell_col, ec.data(), sizeof(int) * ec.size(), cudaMemcpyHostToDevice) ||
+          cudaMemcpy(a->ell_val, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice)) {
+        bd_csr_destroy(a);
+        return fail(ctx, BD_ECUDA, "bd_csr_create: ELL allocation/copy failed");
+      }
+      a->ell_w = W;
+    }
+  }
   *out = a;
   return BD_OK;
 }
 
 bd_status bd_csr_destroy(bd_csr* a) {
   if (!a) return BD_OK;
+  cudaFree(a->ell_col);
+  cudaFree(a->ell_val);
   cudaFree(a->rowptr);
   cudaFree(a->col);
   cudaFree(a->val);
@@ -1730,12 +1757,41 @@ bd_status bd_spmv(bd_csr* a, const double* x, double* y, double alpha, double be
   if (!a) return BD_EINVAL;
   bd_ctx* ctx = a->ctx;
   Scope sc(ctx);
+  if (a->ell_w) {
+    const int grid = grid_for(ctx, a->nrows, dev::TPB);
+    switch (a->ell_w) {
+      case 8: dev::k_spmv_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta); break;
+      case 16: dev::k_spmv_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta); break;
+      case 24: dev::k_spmv_ell<24><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta); break;
+      default: dev::k_spmv_ell<32><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta);
+    }
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   const int grid = grid_for(ctx, a->nrows, dev::TPB / a->G);
   switch (a->G) {
     case 4: dev::k_spmv<4><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
     case 8: dev::k_spmv<8><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
     case 16: dev::k_spmv<16><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta); break;
     default: dev::k_spmv<32><<<grid, dev::TPB, 0, ctx->stream>>>(a->dev(), x, y, alpha, beta);
+  }
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_spmv_split(bd_csr* a, const double* x, int64_t nsplit, const double* x_ghost,
+                        double* y, double alpha, double beta) {
+  if (!a || !x || !y || nsplit < 0 || (nsplit < a->ncols && !x_ghost)) return BD_EINVAL;
+  bd_ctx* ctx = a->ctx;
+  if (!a->ell_w) return fail(ctx, BD_EINVAL, "bd_spmv_split: matrix has no ELL copy (rows too long)");
+  Scope sc(ctx);
+  const int grid = grid_for(ctx, a->nrows, dev::TPB);
+  const int ns = (int)std::min<int64_t>(nsplit, 0x7fffffff);
+  switch (a->ell_w) {
+    case 8: dev::k_spmv_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns); break;
+    case 16: dev::k_spmv_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns); break;
+    case 24: dev::k_spmv_ell<24><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns); break;
+    default: dev::k_spmv_ell<32><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns);
   }
   LAUNCHED(ctx);
   return BD_OK;

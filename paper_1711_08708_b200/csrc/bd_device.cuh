@@ -306,6 +306,41 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr a, const double* __restrict__ 
   }
 }
 
+// Generic SpMV on the entry-major ELL copy of a CSR matrix with short,
+// near-uniform rows (P1 stencils): one thread per row, W entries in chunks of
+// 8 with all loads of a chunk issued before the FMAs; padding entries have
+// column -1.  Row sums run in column order, like the CSR kernels.
+// x split in two arrays (sharded ranks: owned entries, then the ghost halo):
+// column c reads x[c] for c < nsplit and x2[c - nsplit] otherwise.
+template <int W>
+__global__ void __launch_bounds__(TPB) k_spmv_ell(int64_t nrows, const int* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ x, double* y,
+                                                  double alpha, double beta,
+                                                  const double* __restrict__ x2 = nullptr,
+                                                  int nsplit = 0x7fffffff) {
+  for (int64_t r = blockIdx.x * (int64_t)TPB + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * TPB) {
+    double s = 0.0;
+#pragma unroll
+    for (int e0 = 0; e0 < W; e0 += 8) {
+      int cl[8];
+      double a[8], xv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cl[e] = __ldg(&col[(int64_t)(e0 + e) * nrows + r]);
+        a[e] = __ldg(&val[(int64_t)(e0 + e) * nrows + r]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        xv[e] = cl[e] < 0 ? 0.0 : (cl[e] < nsplit ? __ldg(&x[cl[e]]) : __ldg(&x2[cl[e] - nsplit]));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s = fma(a[e], xv[e], s);
+    }
+    y[r] = (beta == 0.0) ? alpha * s : fma(beta, y[r], alpha * s);
+  }
+}
+
 // q = Λ x (bd/system.py:106-116) with optional x·q (the PCG curvature d·q):
 //   top    = S_1 u ; top[:m] += S_i v
 //   bottom = (S_i u[:m] + S_i v) + γ (M_H ∘ v)

@@ -219,31 +219,41 @@ class DistributedSystem:
     def m(self):
         return self.lp.m_own
 
-    def ext_u(self, u):
-        lp = self.lp
-        g = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size, "u")
-        return _torch().cat([u, g]), g
-
-    def ext_heart(self, v_own, ghost_heart):
-        return _torch().cat([v_own, ghost_heart])
-
     def heart_ghosts(self, v):
         lp = self.lp
         return self.comm.halo(v, lp.send_heart, lp.recv_heart, lp.m_ghost, "h")
 
+    def spmv_split(self, a, x, nsplit, x_ghost, out=None):
+        """a @ [x[:nsplit] ; x_ghost] without concatenating (native backend:
+        bd_spmv_split); backends without it (the CPU test double) concatenate."""
+        f = getattr(self.be, "spmv_split", None)
+        if f is not None:
+            return f(a, x, nsplit, x_ghost, out)
+        y = self.be.spmv(a, _torch().cat([x[:nsplit], x_ghost]))
+        if out is None:
+            return y
+        out.copy_(y)
+        return out
+
     def apply(self, x):
-        """q = Λ x (bd/system.py:106-116) with halo exchanges of u and v."""
+        """q = Λ x (bd/system.py:106-116) with halo exchanges of u and v.
+        Local columns are [owned | ghosts] for S_1 and [owned heart | ghost
+        heart] for S_i; heart vertices lead both the owned and the ghost lists,
+        so the S_i products read u and v with a split at m_own."""
         lp = self.lp
-        u, v = x[: lp.n_own], x[lp.n_own:]
-        ue, ug = self.ext_u(u)
-        ve = self.ext_heart(v, self.heart_ghosts(v))
-        ue_h = self.ext_heart(u[: lp.m_own], ug[: lp.m_ghost])
-        iv = self.be.spmv(self.Si, ve)
-        iu = self.be.spmv(self.Si, ue_h)
-        top = self.be.spmv(self.S1, ue)
-        top[: lp.m_own] += iv
-        bottom = iu + iv + lp.gamma * (self.mh * v)
-        return _torch().cat([top, bottom])
+        n, m = lp.n_own, lp.m_own
+        u, v = x[:n], x[n:]
+        ug = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size, "u")
+        vg = self.heart_ghosts(v)
+        q = _torch().empty_like(x)
+        iv = self.spmv_split(self.Si, v, m, vg)
+        self.spmv_split(self.S1, u, n, ug, out=q[:n])
+        q[:m] += iv
+        qv = q[n:]
+        self.spmv_split(self.Si, u, m, ug, out=qv)
+        qv += iv
+        qv += lp.gamma * (self.mh * v)
+        return q
 
     def dot_t(self, a, b):
         """Global a·b as a device 0-d tensor."""
@@ -290,14 +300,14 @@ class DistributedBlockLU:
         s, lp = self.s, self.s.lp
         ru, rv = r[: lp.n_own], r[lp.n_own:]
         t = self.bulk_inverse(ru)
-        th = s.ext_heart(t[: lp.m_own], s.heart_ghosts(t[: lp.m_own]))  # collective on all ranks
+        tg = s.heart_ghosts(t[: lp.m_own])  # collective on all ranks
         self.si += 1
         self.pk += 1
-        sv = s.be.inner_apply(self.schur, rv - s.be.spmv(s.Si, th))
+        sv = s.be.inner_apply(self.schur, rv - s.spmv_split(s.Si, t, lp.m_own, tg))
         sg = s.heart_ghosts(sv)
         self.si += 1
         corr = _torch().zeros_like(ru)
-        corr[: lp.m_own] = s.be.spmv(s.Si, s.ext_heart(sv, sg))
+        s.spmv_split(s.Si, sv, lp.m_own, sg, out=corr[: lp.m_own])
         u = t - self.bulk_inverse(corr)
         return _torch().cat([u, sv])
 
@@ -447,6 +457,9 @@ class NativeBackend:
 
     def spmv(self, h, x):
         return h.matvec(x.contiguous())
+
+    def spmv_split(self, h, x, nsplit, x_ghost, out=None):
+        return h.matvec_split(x.contiguous(), nsplit, x_ghost.contiguous(), y=out)
 
     def inner(self, kind, a, coords=None):
         from .precond import make_inner

@@ -259,6 +259,15 @@ class NativeCsr:
                    self.ctx.handle)
         return y
 
+    def matvec_split(self, x, nsplit: int, x_ghost, y=None, alpha=1.0, beta=0.0):
+        """y = alpha * A [x[:nsplit] ; x_ghost] + beta * y (bd_spmv_split)."""
+        torch = _torch()
+        if y is None:
+            y = torch.zeros(self.shape[0], dtype=torch.float64, device=x.device)
+        _lib.check(_lib.lib().bd_spmv_split(self.handle, _lib.ptr(x), int(nsplit), _lib.ptr(x_ghost),
+                                            _lib.ptr(y), alpha, beta), self.ctx.handle)
+        return y
+
     def __del__(self):
         try:
             if _lib._lib is not None and getattr(self, "handle", None):
