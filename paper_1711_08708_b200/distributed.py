@@ -539,11 +539,50 @@ def ghost_sets(mesh, part: np.ndarray, nprocs: int):
     return out
 
 
+def _rows_device(mesh, params, fibers, owned, m_own):
+    """(S1, Si, Sm, mass, mh) of the owned rows, global columns, like
+    `_rows_csr` / `_rows_mass` but assembled on the GPU: the elements touching
+    owned vertices form a local mesh (owned + one ghost layer, renumbered
+    heart-first), `DeviceAssembler` assembles it, and the owned rows are mapped
+    back to global columns.  Owned rows are complete (every element touching
+    an owned vertex is in the local mesh); ghost rows are discarded."""
+    from .assembly import DeviceAssembler, Space
+    from .mesh import Mesh
+
+    n, m = mesh.vertex_count, mesh.heart_vertex_count
+    pos = np.zeros(n, dtype=bool)
+    pos[owned] = True
+    touch = pos[mesh.elements].any(axis=1)
+    el = mesh.elements[touch]
+    verts = np.unique(el)                               # ascending global ids
+    lv = np.concatenate([verts[verts < m], verts[verts >= m]])  # heart-first (already sorted)
+    g2L = -np.ones(n, dtype=np.int64)
+    g2L[lv] = np.arange(lv.size)
+    hv = int((lv < m).sum())
+    local = Mesh(mesh.dim, np.ascontiguousarray(mesh.vertices[lv]), g2L[el],
+                 np.asarray(mesh.tags)[touch], hv)
+    da = DeviceAssembler(local, params, fibers)
+
+    def back(a, rows, cols_global, nglob):
+        a = a[g2L[rows]].tocsr()
+        out = sp.csr_matrix((a.data, cols_global[a.indices], a.indptr), shape=(rows.size, nglob))
+        out.sort_indices()
+        return out
+
+    S1 = back(da.stiffness("bar1"), owned, lv, n)
+    Si = back(da.stiffness("intra"), owned[:m_own], lv[:hv], m)
+    Sm = back(da.stiffness("mono"), owned[:m_own], lv[:hv], m)
+    mass = da.lumped_mass(Space.FULL)[g2L[owned]]
+    mh = da.lumped_mass(Space.HEART_ONLY)[g2L[owned[:m_own]]]
+    return S1, Si, Sm, mass, mh
+
+
 def build_local_from_mesh(mesh, params, fibers, dt, part: np.ndarray, rank: int, nprocs: int,
-                          comm_allreduce=None) -> "LocalProblem":
+                          comm_allreduce=None, assembly: str = "host") -> "LocalProblem":
     """The rank-local problem assembled from the elements touching the owned
-    vertices only.  beta (mean diagonal of S_1, bd/precond.py:79-81) needs a
-    global sum: comm_allreduce(list) -> list (None: single process)."""
+    vertices only (assembly="device": on the GPU, `_rows_device`).  beta (mean
+    diagonal of S_1, bd/precond.py:79-81) needs a global sum:
+    comm_allreduce(list) -> list (None: single process)."""
     from .assembly import Space
     from .conductivity import TensorField
     from .system import gamma as gamma_fn
@@ -554,11 +593,16 @@ def build_local_from_mesh(mesh, params, fibers, dt, part: np.ndarray, rank: int,
     ghosts_all = ghost_sets(mesh, part, nprocs)
     ghosts = ghosts_all[rank]
     m_own, m_ghost = int((owned < m).sum()), int((ghosts < m).sum())
-    S1 = _rows_csr(mesh, TensorField(params, d, "bar1", fibers), Space.FULL, owned, n)
-    Si = _rows_csr(mesh, TensorField(params, d, "intra", fibers), Space.HEART_ONLY, owned[:m_own], m)
-    Sm = _rows_csr(mesh, TensorField(params, d, "mono", fibers), Space.HEART_ONLY, owned[:m_own], m)
-    mass = _rows_mass(mesh, Space.FULL, owned)
-    mh = _rows_mass(mesh, Space.HEART_ONLY, owned[:m_own])
+    if assembly == "device":
+        S1, Si, Sm, mass, mh = _rows_device(mesh, params, fibers, owned, m_own)
+    else:
+        S1 = _rows_csr(mesh, TensorField(params, d, "bar1", fibers), Space.FULL, owned, n)
+        Si = _rows_csr(mesh, TensorField(params, d, "intra", fibers), Space.HEART_ONLY,
+                       owned[:m_own], m)
+        Sm = _rows_csr(mesh, TensorField(params, d, "mono", fibers), Space.HEART_ONLY,
+                       owned[:m_own], m)
+        mass = _rows_mass(mesh, Space.FULL, owned)
+        mh = _rows_mass(mesh, Space.HEART_ONLY, owned[:m_own])
     diag_sum = float(S1[np.arange(owned.size), owned].sum())
     tot = comm_allreduce([diag_sum]) if comm_allreduce else [diag_sum]
     beta = tot[0] / n
@@ -615,7 +659,8 @@ class DistributedSimulation:
         self.wl = wl
         self.comm = Comm(dist, device)
         self.lp = build_local_from_mesh(wl.mesh, wl.params, wl.fibers, wl.dt, part, rank, nprocs,
-                                        comm_allreduce=self.comm.allreduce)
+                                        comm_allreduce=self.comm.allreduce,
+                                        assembly=os.environ.get("BD_ASSEMBLY", "device"))
         self.backend = NativeBackend()
         self.dsys = DistributedSystem(self.lp, self.comm, self.backend)
         self.prec = DistributedBlockLU(self.dsys, inner or wl.inner, self.lp.beta)
