@@ -41,6 +41,30 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# The JSON line is the only thing on stdout: libraries that write to fd 1
+# (NCCL's version banner at communicator creation, CUDA/driver notices) are
+# pointed at stderr, and the result goes to a private copy of the original fd.
+_RESULT_FD = None
+
+
+def _claim_stdout():
+    global _RESULT_FD
+    if _RESULT_FD is None:
+        sys.stdout.flush()
+        _RESULT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    """Write the one result line to the original stdout."""
+    data = (json.dumps(obj) + "\n").encode()
+    if _RESULT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, data)
+
+
 def measured_peak_hbm():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -318,7 +342,7 @@ def run_native(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "setup_s": {"assembly": round(t_asm, 1), "precond": round(t_setup, 2)},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def weak_cells(base, world):
@@ -386,7 +410,7 @@ def run_sharded(args, rank, world, local_rank):
     steps_s = args.steps / (ms / 1e3)
     value = steps_s * (n + m) / base_dof  # cfg2-equivalent time steps per second (aggregate)
     if rank == 0:
-        print(json.dumps({
+        emit(({
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -399,7 +423,7 @@ def run_sharded(args, rank, world, local_rank):
                        "pcg_loop": "cuda graph" if graph_used else f"eager ({graph_err})",
                        "parallelism": f"mesh partition x{world}"},
             "gpu_launches": int(ctx.launches() - launches0), "clocks": clk,
-            "setup_s": round(t_setup, 1)}), flush=True)
+            "setup_s": round(t_setup, 1)}))
 
 
 def cpu_baseline(sysm, km, wl, iters_per_step, n_iter):
@@ -514,10 +538,11 @@ def run_reference(args, rank):
             "e2e": {"value": round(value, 6) if value else None, "unit": UNIT,
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_s": {"assembly": round(t_asm, 1)}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
