@@ -256,8 +256,8 @@ class DistributedSystem:
         return q
 
     def dot_t(self, a, b):
-        """Global a·b as a device 0-d tensor."""
-        return self.comm.allreduce_((a * b).sum().reshape(1))[0]
+        """Global a·b as a device 0-d tensor (one fused dot per rank)."""
+        return self.comm.allreduce_(_torch().dot(a, b).reshape(1))[0]
 
     def mean_u_t(self, u):
         return self.comm.allreduce_(u.sum().reshape(1))[0] / self.lp.n_global
@@ -287,6 +287,7 @@ class DistributedBlockLU:
         self.bulk = be.inner(inner, lp.bulk_block, None if xyz is None else xyz)
         self.schur = be.inner(inner, lp.schur_block, None if xyz is None else xyz[: lp.m_own])
         self.p1 = self.pk = self.si = 0
+        self._corr = None  # pad(S_i s): torso rows stay zero, heart rows rewritten per apply
 
     def bulk_inverse(self, y):
         self.p1 += 1
@@ -306,7 +307,9 @@ class DistributedBlockLU:
         sv = s.be.inner_apply(self.schur, rv - s.spmv_split(s.Si, t, lp.m_own, tg))
         sg = s.heart_ghosts(sv)
         self.si += 1
-        corr = _torch().zeros_like(ru)
+        if self._corr is None or self._corr.shape != ru.shape or self._corr.device != ru.device:
+            self._corr = _torch().zeros_like(ru)
+        corr = self._corr
         s.spmv_split(s.Si, sv, lp.m_own, sg, out=corr[: lp.m_own])
         u = t - self.bulk_inverse(corr)
         return _torch().cat([u, sv])
@@ -375,8 +378,8 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
         S["bad"].logical_or_(brk)
         go = active & ~brk
         alpha = torch.where(go, rho / dq, zero)
-        S["x"].add_(alpha * d)
-        S["r"].sub_(alpha * q)
+        S["x"].addcmul_(d, alpha)
+        S["r"].addcmul_(q, alpha, value=-1.0)
         S["iters"].add_(go.to(torch.int64))
         relk = torch.sqrt(dsys.dot_t(S["r"], S["r"])) / nb
         S["k"].add_(1)

@@ -12,8 +12,9 @@ t0 = time.perf_counter()
 b = configs.BUILDERS[a.workload]
 wl = b(int(a.cells)) if a.cells else b()
 if a.inner: wl.inner = a.inner
-sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
-km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+sysm = bd.BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False,
+                               assembly="device")
+km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers, assembly="device")
 t1 = time.perf_counter()
 pre = bd.BlockLUPreconditioner(sysm, inner=wl.inner, monodomain_matrix=km)
 t2 = time.perf_counter()
