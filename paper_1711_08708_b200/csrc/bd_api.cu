@@ -169,6 +169,11 @@ struct DevBTile {
 };
 
 struct DevSuper {
+  double* pinv = nullptr;    // panel inverses of the big supernodes' dense blocks
+  int* sn_pan = nullptr;
+  int* task_kind = nullptr;  // forward: split external phases (nullptr: none)
+  int* task_arg = nullptr;
+  int* sn_cnt = nullptr;
   int* sn_start = nullptr;
   int* sn_size = nullptr;
   int* task_sn = nullptr;
@@ -191,6 +196,7 @@ struct bd_inner {
   bool btile = false;
   DevBTile BL, BU;
   double* rtmp = nullptr;
+  double* rext = nullptr;  // supernodal forward: precomputed external phases (n)
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
   bool persist = false;
@@ -587,7 +593,18 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
       lvb[s] = lv;
     }
   }
-  auto order = [&](const std::vector<int32_t>& lv, DevSuper* out) -> bd_status {
+  // external entries of each supernode's rows (forward: columns < start)
+  std::vector<int64_t> ext(ns, 0);
+  for (int64_t sn = 0; sn < ns; ++sn)
+    for (int64_t i = start[sn]; i < start[sn] + size[sn]; ++i)
+      ext[sn] += L.indptr[i + 1] - L.indptr[i] - 1 - (i - start[sn]);
+  const int64_t split_min = getenv("BD_SUPER_SPLIT") ? atoll(getenv("BD_SUPER_SPLIT")) : 8192;
+  // dense block of supernode sn: D[k][j] (j <= k) = L[start+k][start+j], the
+  // last k+1 entries of the row (diagonal last)
+  auto dense = [&](int64_t c0, int64_t k, int64_t j) -> long double {
+    return L.values[L.indptr[c0 + k + 1] - 1 - k + j];
+  };
+  auto order = [&](const std::vector<int32_t>& lv, DevSuper* out, bool split) -> bd_status {
     std::vector<int32_t> idx(ns);
     std::iota(idx.begin(), idx.end(), 0);
     std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return lv[a] < lv[b]; });
@@ -596,27 +613,93 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
       st[k] = start[idx[k]];
       sz[k] = size[idx[k]];
     }
-    // tasks: a big supernode alone, or up to 16 small ones of the same level
+    // tasks: a big supernode alone, or up to 16 small ones of the same level.
+    // Forward: a big supernode with a heavy external phase (the separators of
+    // a nested-dissection factor, whose rows carry the fill of their whole
+    // subtree) gets its external phase split into SN_CHUNK-row chunk tasks
+    // placed right before it, so many CTAs stream it; the supernode's own task
+    // then waits for its chunks and does the dense phase.
+    std::vector<int32_t> kind, arg;
+    bool any_split = false;
     for (int64_t k = 0; k < ns;) {
-      tasks.push_back((int32_t)k);
       if (sz[k] > 32) {
+        if (split && ext[idx[k]] >= split_min) {
+          const int nch = (sz[k] + dev::SN_CHUNK - 1) / dev::SN_CHUNK;
+          for (int ch = 0; ch < nch; ++ch) {
+            tasks.push_back((int32_t)k);
+            kind.push_back(1);
+            arg.push_back(ch * dev::SN_CHUNK);
+          }
+          tasks.push_back((int32_t)k);
+          kind.push_back(2);
+          arg.push_back(nch);
+          any_split = true;
+        } else {
+          tasks.push_back((int32_t)k);
+          kind.push_back(0);
+          arg.push_back(0);
+        }
         ++k;
         continue;
       }
+      tasks.push_back((int32_t)k);
+      kind.push_back(0);
+      arg.push_back(0);
       int64_t e = k + 1;
       while (e < ns && e - k < 16 && sz[e] <= 32 && lv[idx[e]] == lv[idx[k]]) ++e;
       k = e;
     }
     tasks.push_back((int32_t)ns);
+    // inverses of the 32x32 diagonal blocks of every panel of the big
+    // supernodes, in solve order (forward: rows ascending, B = D[P][P];
+    // backward, U = L^T: rows descending, B[l][m] = D[q-m][q-l] with
+    // q = ns-1-p0), each padded to 32x32, in long double
+    if (!getenv("BD_SUPER_NOPINV")) {
+      std::vector<int32_t> pan(ns, -1);
+      std::vector<double> pinv;
+      std::vector<long double> B(32 * 32), X(32 * 32);
+      const bool fwd = out == fw;
+      for (int64_t k = 0; k < ns; ++k) {
+        if (sz[k] <= 32) continue;
+        pan[k] = (int32_t)(pinv.size() / 1024);
+        const int64_t c0 = st[k], nsz = sz[k];
+        for (int64_t p0 = 0; p0 < nsz; p0 += 32) {
+          const int pn = (int)std::min<int64_t>(32, nsz - p0);
+          for (int l = 0; l < pn; ++l)
+            for (int m = 0; m <= l; ++m)
+              B[l * 32 + m] = fwd ? dense(c0, p0 + l, p0 + m)
+                                  : dense(c0, nsz - 1 - p0 - m, nsz - 1 - p0 - l);
+          std::fill(X.begin(), X.end(), 0.0L);
+          for (int l = 0; l < pn; ++l) {  // X = B^{-1}, lower triangular
+            for (int m = 0; m <= l; ++m) {
+              long double acc = (l == m) ? 1.0L : 0.0L;
+              for (int j = m; j < l; ++j) acc -= B[l * 32 + j] * X[j * 32 + m];
+              X[l * 32 + m] = acc / B[l * 32 + l];
+            }
+          }
+          for (int q = 0; q < 1024; ++q) pinv.push_back((double)X[q]);
+        }
+      }
+      if (!pinv.empty()) {
+        CK(ctx, upload_vec(&out->pinv, pinv));
+        CK(ctx, upload_vec(&out->sn_pan, pan));
+      }
+    }
     CK(ctx, upload_vec(&out->sn_start, st));
     CK(ctx, upload_vec(&out->sn_size, sz));
     CK(ctx, upload_vec(&out->task_sn, tasks));
+    if (any_split) {
+      CK(ctx, upload_vec(&out->task_kind, kind));
+      CK(ctx, upload_vec(&out->task_arg, arg));
+      std::vector<int32_t> zeros(ns, 0);
+      CK(ctx, upload_vec(&out->sn_cnt, zeros));
+    }
     out->ntasks = (int)tasks.size() - 1;
     out->grid = (int)std::max<int64_t>(1, std::min<int64_t>(out->ntasks, (int64_t)ctx->nsm * 2));
     return BD_OK;
   };
-  TRY(order(lvf, fw));
-  TRY(order(lvb, bw));
+  TRY(order(lvf, fw, !getenv("BD_SUPER_NOSPLIT")));
+  TRY(order(lvb, bw, false));
   if (getenv("BD_DEBUG")) {
     int64_t big = 0, maxsz = 0, rows_big = 0;
     for (int64_t s = 0; s < ns; ++s) {
@@ -638,6 +721,11 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
 }
 
 void free_super(DevSuper* s) {
+  cudaFree(s->pinv);
+  cudaFree(s->sn_pan);
+  cudaFree(s->task_kind);
+  cudaFree(s->task_arg);
+  cudaFree(s->sn_cnt);
   cudaFree(s->sn_start);
   cudaFree(s->sn_size);
   cudaFree(s->task_sn);
@@ -1302,14 +1390,18 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(p->y_int, p->n, dev::SENTINEL, c);
     LAUNCHED(ctx);
     dev::SuperTri tl{(int)p->n,        p->L.rowptr,  p->L.col,    p->L.val, p->SL.sn_start,
-                     p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr};
+                     p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr,
+                     p->SL.task_kind,   p->SL.task_arg, p->SL.sn_cnt, p->rext,
+                     p->SL.pinv,        p->SL.sn_pan};
     dev::k_trsv_super<true, Rhs><<<p->SL.grid, 512, 0, st>>>(tl, rhs, p->y_int, nullptr, c, ctr0,
                                                               ctr0 + 1);
     LAUNCHED(ctx);
     dev::k_fill<<<grid_for(ctx, p->n, dev::TPB), dev::TPB, 0, st>>>(x_int, p->n, dev::SENTINEL, c);
     LAUNCHED(ctx);
     dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
-                     p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm};
+                     p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm,
+                     nullptr,           nullptr,        nullptr,      nullptr,
+                     p->SU.pinv,        p->SU.sn_pan};
     dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
         tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
     LAUNCHED(ctx);
@@ -2015,6 +2107,8 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
     const char* m = getenv("BD_EXACT_TRSV");
     if (!(m && std::string(m) == "rows")) {
       st = build_super(ctx, lower, &p->SL, &p->SU);
+      if (st == BD_OK && p->SL.task_kind && dalloc(&p->rext, lower.n))
+        st = fail(ctx, BD_ECUDA, "supernodal solve: allocation failed");
       if (st == BD_OK) p->super = true;
     }
   }
@@ -2088,6 +2182,7 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_btile(&p->BU);
 
   cudaFree(p->rtmp);
+  cudaFree(p->rext);
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);

@@ -1731,9 +1731,23 @@ struct SuperTri {
   int ntasks;           // a task is either ONE big supernode (> 32 rows) or up to
                         // 16 small independent ones (same level), one per warp
   const int* perm;      // nullable: scatter of the output (original order)
+  // split external phase of big forward supernodes (nullable): task_kind 1 =
+  // chunk of SN_CHUNK rows (first row task_arg) whose b - L_ext x_ext goes to
+  // rext; task_kind 2 = the supernode's dense phase, waiting for task_arg
+  // chunks on sn_cnt[supernode]
+  const int* task_kind;
+  const int* task_arg;
+  int* sn_cnt;
+  double* rext;
+  // dense phase of big supernodes (nullable): inverses of the 32x32 diagonal
+  // blocks of every panel, in solve order, pinv[(panel*32 + l)*32 + m], the
+  // supernode's first panel at sn_pan[supernode]
+  const double* pinv;
+  const int* sn_pan;
 };
 
 constexpr int SN_MAX = 1024;
+constexpr int SN_CHUNK = 64;  // rows per external-phase chunk (16 warps x RW 4)
 
 // One warp solves one small supernode (<= 32 rows): external dots RW rows at
 // a time, then the dense triangle with the coefficients in registers.
@@ -1814,6 +1828,61 @@ __device__ __forceinline__ void super_small_warp(const SuperTri& t, const Rhs& r
   }
 }
 
+// External phase of a big supernode: r[k] = b_k - L_k,ext x_ext for rows
+// [kbeg, kend) of the supernode (c0, c1), RW rows per warp in flight, each
+// row's entries lane-strided and combined with a warp sum.  dst is indexed by
+// the row offset k (shared r, or rext + c0 for a chunk task).
+template <bool LOWER, int RW, class Rhs>
+__device__ __forceinline__ void super_ext_rows(const SuperTri& t, const Rhs& rhs,
+                                               double* __restrict__ x, int c0, int c1, int kbeg,
+                                               int kend, double* dst) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k0 = kbeg + warp * RW; k0 < kend; k0 += nw * RW) {
+    int eb[RW], ee[RW];
+    double sacc[RW];
+#pragma unroll
+    for (int u = 0; u < RW; ++u) {
+      const int k = k0 + u;
+      sacc[u] = 0.0;
+      eb[u] = ee[u] = 0;
+      if (k < kend) {
+        const int i = c0 + k;
+        const int b = t.rowptr[i], e = t.rowptr[i + 1];
+        eb[u] = LOWER ? b : b + (c1 - i);
+        ee[u] = LOWER ? e - 1 - k : e;
+      }
+    }
+    int len = 0;
+#pragma unroll
+    for (int u = 0; u < RW; ++u) len = max(len, ee[u] - eb[u]);
+    for (int q = lane; q < len; q += 32) {
+      int cl[RW];
+      double vl[RW], xv[RW];
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        const bool ok = eb[u] + q < ee[u];
+        cl[u] = ok ? t.col[eb[u] + q] : -1;
+        vl[u] = ok ? t.val[eb[u] + q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < RW; ++u) xv[u] = ld_relaxed_if(&x[cl[u] < 0 ? 0 : cl[u]], cl[u] >= 0);
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        double d = xv[u];
+        if (cl[u] >= 0 && __double_as_longlong(d) == SENTINEL) d = spin_load(&x[cl[u]]);
+        sacc[u] = fma(vl[u], d, sacc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RW; ++u) {
+      const double sum = group_sum<32>(sacc[u]);
+      const int k = k0 + u;
+      const double bi = rhs.template eval<32>(k < kend ? c0 + k : -1, lane);
+      if (lane == 0 && k < kend) dst[k] = __dsub_rn(bi, sum);
+    }
+  }
+}
+
 template <bool LOWER, class Rhs>
 __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double* __restrict__ x,
                                                     double* __restrict__ out, Ctl c, int ctr_task,
@@ -1832,8 +1901,22 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
     __syncthreads();
     if (task >= t.ntasks) break;
     const int s0 = t.task_sn[task], s1 = t.task_sn[task + 1];
+    const int kind = t.task_kind ? t.task_kind[task] : 0;
+    if (kind == 1) {  // external-phase chunk of a big supernode
+      const int c0 = t.sn_start[s0], ns = t.sn_size[s0];
+      const int kb = t.task_arg[task], ke = min(ns, kb + SN_CHUNK);
+      super_ext_rows<LOWER, RW>(t, rhs, x, c0, c0 + ns, kb, ke, t.rext + c0);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(t.sn_cnt + s0, 1);
+      }
+      continue;
+    }
     unsigned long long t_beg = 0;
-    unsigned long long* trace = g_tile_trace;
+    // trace (debug): steps > 0 traces the backward passes, < 0 the forward ones
+    const int tsteps = g_tile_trace_steps < 0 ? -g_tile_trace_steps : g_tile_trace_steps;
+    unsigned long long* trace = ((g_tile_trace_steps < 0) == LOWER) ? g_tile_trace : nullptr;
     if (trace && threadIdx.x == 0) t_beg = gtimer();
     if (s1 - s0 > 1 || t.sn_size[s0] <= 32) {
       // group of small independent supernodes: one warp each, no CTA barrier
@@ -1841,7 +1924,7 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
         super_small_warp<LOWER>(t, rhs, x, out, t.sn_start[s0 + warp], t.sn_size[s0 + warp], lane);
       if (trace) {
         __syncthreads();
-        if (threadIdx.x == 0 && task < g_tile_trace_steps) {
+        if (threadIdx.x == 0 && task < tsteps) {
           trace[task * 4 + 0] = t_beg;
           trace[task * 4 + 1] = gtimer();
           trace[task * 4 + 2] = blockIdx.x;
@@ -1851,50 +1934,20 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
       continue;
     }
     const int c0 = t.sn_start[s0], ns = t.sn_size[s0], c1 = c0 + ns;
-    // (1) right-hand side minus the external part, RW rows per warp in flight
-    for (int k0 = warp * RW; k0 < ns; k0 += nw * RW) {
-      int eb[RW], ee[RW];
-      double sacc[RW];
-#pragma unroll
-      for (int u = 0; u < RW; ++u) {
-        const int k = k0 + u;
-        sacc[u] = 0.0;
-        eb[u] = ee[u] = 0;
-        if (k < ns) {
-          const int i = c0 + k;
-          const int b = t.rowptr[i], e = t.rowptr[i + 1];
-          eb[u] = LOWER ? b : b + (c1 - i);
-          ee[u] = LOWER ? e - 1 - k : e;
-        }
+    if (kind == 2) {
+      // (1) precomputed by the chunk tasks: wait for them, then stage r
+      if (threadIdx.x == 0) {
+        const volatile int* cnt = t.sn_cnt + s0;
+        while (*cnt < t.task_arg[task]) __nanosleep(64);
+        t.sn_cnt[s0] = 0;  // ready for the next pass
+        __threadfence();
       }
-      int len = 0;
-#pragma unroll
-      for (int u = 0; u < RW; ++u) len = max(len, ee[u] - eb[u]);
-      for (int q = lane; q < len; q += 32) {
-        int cl[RW];
-        double vl[RW], xv[RW];
-#pragma unroll
-        for (int u = 0; u < RW; ++u) {
-          const bool ok = eb[u] + q < ee[u];
-          cl[u] = ok ? t.col[eb[u] + q] : -1;
-          vl[u] = ok ? t.val[eb[u] + q] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < RW; ++u) xv[u] = ld_relaxed_if(&x[cl[u] < 0 ? 0 : cl[u]], cl[u] >= 0);
-#pragma unroll
-        for (int u = 0; u < RW; ++u) {
-          double d = xv[u];
-          if (cl[u] >= 0 && __double_as_longlong(d) == SENTINEL) d = spin_load(&x[cl[u]]);
-          sacc[u] = fma(vl[u], d, sacc[u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < RW; ++u) {
-        const double sum = group_sum<32>(sacc[u]);
-        const int k = k0 + u;
-        const double bi = rhs.template eval<32>(k < ns ? c0 + k : -1, lane);
-        if (lane == 0 && k < ns) r[k] = __dsub_rn(bi, sum);
-      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < ns; k += blockDim.x)
+        r[k] = ld_relaxed_if(&t.rext[c0 + k], true);
+    } else {
+      // (1) right-hand side minus the external part, RW rows per warp in flight
+      super_ext_rows<LOWER, RW>(t, rhs, x, c0, c1, 0, ns, r);
     }
     __syncthreads();
     unsigned long long t_ext = 0;
@@ -1903,6 +1956,17 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
     //     for L, descending for U).  r[k] holds row k's rhs, then its solution.
     for (int p0 = 0; p0 < ns; p0 += 32) {
       const int pn = min(32, ns - p0);
+      // panel inverse rows of this warp (rows warp, warp + nw), loaded before
+      // the update so their latency hides behind it
+      double pv[2] = {0.0, 0.0};
+      const double* pinv = t.pinv ? t.pinv + ((int64_t)t.sn_pan[s0] + p0 / 32) * 1024 : nullptr;
+      if (pinv) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = warp + h * nw;
+          if (l < pn && lane <= l) pv[h] = __ldg(&pinv[l * 32 + lane]);
+        }
+      }
       // (a) panel rows minus the already solved rows [0, p0) of the block
       if (p0 > 0) {
         for (int w = warp; w < pn; w += nw) {
@@ -1921,8 +1985,30 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
         }
         __syncthreads();
       }
-      // (b) the panel triangle, one warp, coefficients in shared memory
-      if (warp == 0) {
+      // (b) the panel triangle
+      if (pinv) {
+        // precomputed block inverse: x_l = sum_{m<=l} inv[l][m] r_m, one warp per row
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = warp + h * nw;
+          if (l < pn) {
+            const int km = LOWER ? p0 + lane : ns - 1 - (p0 + lane);
+            double v = (lane <= l) ? pv[h] * r[km] : 0.0;
+            v = group_sum<32>(v);
+            if (lane == 0) panel[0][l] = v;
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < pn) {
+          const int k = LOWER ? p0 + threadIdx.x : ns - 1 - (p0 + threadIdx.x);
+          const int i = c0 + k;
+          const double xi = panel[0][threadIdx.x];
+          r[k] = xi;
+          publish(&x[i], xi);
+          if (out) out[t.perm ? t.perm[i] : i] = xi;
+        }
+      } else if (warp == 0) {
+        // one warp, coefficients in shared memory
         const int k = LOWER ? p0 + lane : ns - 1 - (p0 + lane);
         const bool ok = lane < pn;
         const int i = ok ? c0 + k : c0;
@@ -1959,7 +2045,7 @@ __global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double*
       }
       __syncthreads();
     }
-    if (trace && threadIdx.x == 0 && task < g_tile_trace_steps) {
+    if (trace && threadIdx.x == 0 && task < tsteps) {
       trace[task * 4 + 0] = t_beg;
       trace[task * 4 + 1] = gtimer();
       trace[task * 4 + 2] = blockIdx.x;

@@ -1,4 +1,5 @@
-"""Dev tool: per-task trace of the supernodal solve (backward pass of the bulk exact factor, cfg1)."""
+"""Dev tool: per-task trace of the supernodal solve of the bulk exact factor
+(cfg1); argv[1] = "fwd" traces the forward pass, default the backward one."""
 import ctypes as C, os, sys
 import numpy as np
 sys.path.insert(0, '/root/repo')
@@ -9,7 +10,8 @@ from paper_1711_08708_b200.assembly import assemble_stiffness
 from paper_1711_08708_b200.conductivity import TensorField
 from paper_1711_08708_b200.precond import regularize_stiffness
 wl = configs.cfg1()
-g = regularize_stiffness(assemble_stiffness(wl.mesh, TensorField(wl.params, 2, "bar1", wl.fibers))).grounded()
+from paper_1711_08708_b200.assembly import DeviceAssembler
+g = regularize_stiffness(DeviceAssembler(wl.mesh, wl.params, wl.fibers).stiffness("bar1")).grounded()
 inner = bd.ExactFactorization(); inner.setup(g)
 L = _lib.lib(); L.bd_debug_tile_trace.argtypes = [C.c_void_p, C.c_int]
 NT = 200000
@@ -19,7 +21,7 @@ inner.apply_inverse(y); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); inner.apply_inverse(y); e1.record(); torch.cuda.synchronize()
 print("apply (fwd+bwd) ms", e0.elapsed_time(e1))
-L.bd_debug_tile_trace(C.c_void_p(buf.data_ptr()), NT)
+L.bd_debug_tile_trace(C.c_void_p(buf.data_ptr()), -NT if sys.argv[1:2] == ["fwd"] else NT)
 inner.apply_inverse(y); torch.cuda.synchronize()
 L.bd_debug_tile_trace(None, 0)
 tr = buf.view(NT, 4).cpu().numpy()
