@@ -1797,30 +1797,39 @@ __device__ __forceinline__ void super_small_warp(const SuperTri& t, const Rhs& r
   const int k = LOWER ? lane : ns - 1 - lane;
   const int i = ok ? c0 + k : c0;
   double diag = 1.0;
-  double a[32];
   int base = 0;
   if (ok) {
     const int b = t.rowptr[i], e = t.rowptr[i + 1];
     diag = LOWER ? t.val[e - 1] : t.val[b];
     base = LOWER ? (e - 1 - k) : b;
   }
+  // coefficients fetched 8 steps ahead instead of held in 32 registers (keeps
+  // the kernel at 2 CTAs/SM); the loads are off the shuffle chain
+  auto coef = [&](int jj) -> double {
+    if (!(ok && jj < lane)) return 0.0;
+    const int kj = LOWER ? jj : ns - 1 - jj;
+    const int j = c0 + kj;
+    return __ldg(&t.val[LOWER ? base + (j - c0) : base + (j - i)]);
+  };
+  double win[8];
 #pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    a[jj] = 0.0;
-    if (ok && jj < lane) {
-      const int kj = LOWER ? jj : ns - 1 - jj;
-      const int j = c0 + kj;
-      a[jj] = LOWER ? t.val[base + (j - c0)] : t.val[base + (j - i)];
+  for (int u = 0; u < 8; ++u) win[u] = coef(u);
+  for (int j0 = 0; j0 < ns; j0 += 8) {
+    double nxt[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = coef(j0 + 8 + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int jj = j0 + u;
+      if (jj >= ns) break;
+      const double rj = __shfl_sync(0xffffffffu, ri, jj);
+      const double dj = __shfl_sync(0xffffffffu, diag, jj);
+      const double xj = __ddiv_rn(rj, dj);
+      if (lane == jj) ri = xj;
+      if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(win[u], xj));
     }
-  }
 #pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    if (jj >= ns) break;
-    const double rj = __shfl_sync(0xffffffffu, ri, jj);
-    const double dj = __shfl_sync(0xffffffffu, diag, jj);
-    const double xj = __ddiv_rn(rj, dj);
-    if (lane == jj) ri = xj;
-    if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(a[jj], xj));
+    for (int u = 0; u < 8; ++u) win[u] = nxt[u];
   }
   if (ok) {
     publish(&x[i], ri);
@@ -1884,7 +1893,7 @@ __device__ __forceinline__ void super_ext_rows(const SuperTri& t, const Rhs& rhs
 }
 
 template <bool LOWER, class Rhs>
-__global__ void __launch_bounds__(512) k_trsv_super(SuperTri t, Rhs rhs, double* __restrict__ x,
+__global__ void __launch_bounds__(512, 2) k_trsv_super(SuperTri t, Rhs rhs, double* __restrict__ x,
                                                     double* __restrict__ out, Ctl c, int ctr_task,
                                                     int ctr_done) {
   if (inactive(c)) return;
