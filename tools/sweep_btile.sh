@@ -1,3 +1,3 @@
-# dev: register-tile occupancy at cfg2 and cfg3 sizes
-MODES=btile@reg,btile@rsmem python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply"
-MODES=btile@reg,btile@rsmem python tools/trsv_bench.py 256,256,128 10 2>&1 | grep -E "us per apply"
+# dev: timing experiment, half of each register-tile inverse loaded (wrong results)
+MODES=btile@reg python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply"
+BD_EXP_HALF=1 MODES=btile@reg python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply"
