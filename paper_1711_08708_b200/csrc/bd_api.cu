@@ -197,6 +197,7 @@ struct bd_inner {
   DevBTile BL, BU;
   double* rtmp = nullptr;
   double* rext = nullptr;  // supernodal forward: precomputed external phases (n)
+  double* dense = nullptr; // exact inner, small n: explicit inverse (P A P^T)^{-1}, row-major
   // tiled cooperative schedule (IC(0) factors with short rows)
   bool tiled = false;
   bool persist = false;
@@ -1294,6 +1295,17 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     LAUNCHED(ctx);
     return BD_OK;
   }
+  if (p->dense) {
+    // small exact inner: y = rhs (permuted order), x = X y, out[perm] = x
+    const int grid = grid_for(ctx, p->n, dev::TPB / G);
+    dev::k_rhs_eval<G, Rhs><<<grid, dev::TPB, 0, st>>>((int)p->n, rhs, p->y_int, c);
+    LAUNCHED(ctx);
+    dev::k_dense_gemv<<<grid_for(ctx, p->n, 8), 256, 0, st>>>(p->n, p->dense, p->y_int, x_int, out,
+                                                             p->perm, c);
+    LAUNCHED(ctx);
+    if (fin >= 0) TRY(launch_dot(ctx, x_int, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
+    return BD_OK;
+  }
   if (p->btile && p->BL.tile_rhs) {
     double* xg = (out && !p->perm) ? out : x_int;
     const DevBTile& bl = p->BL;
@@ -2103,7 +2115,43 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   p->G = pick_g(avg - 1.0);
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
-  if (st == BD_OK && kind == BD_INNER_EXACT) {
+  const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 8192;
+  if (st == BD_OK && kind == BD_INNER_EXACT && n <= dense_max) {
+    // explicit inverse of P A P^T from the sparse factor, one column per host
+    // thread (X^T = X up to rounding; row j of X holds the solve with e_j)
+    std::vector<double> X((size_t)n * n);
+    int bad = 0;
+#pragma omp parallel
+    {
+      std::vector<double> w(n);
+#pragma omp for schedule(dynamic, 8)
+      for (int64_t j = 0; j < n; ++j) {
+        std::fill(w.begin(), w.end(), 0.0);
+        w[j] = 1.0;
+        for (int64_t i = j; i < n; ++i) {  // L w = e_j (diagonal last)
+          double acc = w[i];
+          const int64_t b = lower.indptr[i], e = lower.indptr[i + 1] - 1;
+          for (int64_t q = b; q < e; ++q) acc -= lower.values[q] * w[lower.indices[q]];
+          w[i] = acc / lower.values[e];
+        }
+        for (int64_t i = n - 1; i >= 0; --i) {  // L^T x = w (diagonal first)
+          double acc = w[i];
+          const int64_t b = upper.indptr[i], e = upper.indptr[i + 1];
+          for (int64_t q = b + 1; q < e; ++q) acc -= upper.values[q] * w[upper.indices[q]];
+          w[i] = acc / upper.values[b];
+        }
+        for (int64_t i = 0; i < n; ++i) {
+          if (!std::isfinite(w[i])) bad = 1;
+          X[(size_t)j * n + i] = w[i];
+        }
+      }
+    }
+    if (bad) {
+      st = fail(ctx, BD_EPRECOND, "exact inner: non-finite explicit inverse");
+    } else {
+      CK(ctx, upload_vec(&p->dense, X));
+    }
+  } else if (st == BD_OK && kind == BD_INNER_EXACT) {
     const char* m = getenv("BD_EXACT_TRSV");
     if (!(m && std::string(m) == "rows")) {
       st = build_super(ctx, lower, &p->SL, &p->SU);
@@ -2183,6 +2231,7 @@ bd_status bd_inner_destroy(bd_inner* p) {
 
   cudaFree(p->rtmp);
   cudaFree(p->rext);
+  cudaFree(p->dense);
   cudaFree(p->perm);
   cudaFree(p->inv);
   cudaFree(p->y_int);

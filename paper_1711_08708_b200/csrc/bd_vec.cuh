@@ -32,6 +32,48 @@ __global__ void __launch_bounds__(TPB) k_jacobi(int n, const double* __restrict_
   }
 }
 
+// Dense explicit inverse of a small exact inner (n <= BD_EXACT_DENSE_MAX):
+// the right-hand side is evaluated into y (the inner's permuted order, as the
+// Rhs functors index it), then z = X y with X = (P A P^T)^{-1} row-major, one
+// warp per row, lane-strided dot + fixed butterfly (deterministic).  HBM/L2
+// streaming instead of the latency-bound supernodal passes of a tiny factor.
+template <int G, class Rhs>
+__global__ void __launch_bounds__(TPB) k_rhs_eval(int n, Rhs rhs, double* __restrict__ y, Ctl c) {
+  if (inactive(c)) return;
+  const int lane = threadIdx.x % G;
+  const int rpb = TPB / G;
+  for (int64_t base = (int64_t)blockIdx.x * rpb; base < n; base += (int64_t)gridDim.x * rpb) {
+    const int64_t r = base + threadIdx.x / G;
+    const bool ok = r < n;
+    const double b = rhs.template eval<G>(ok ? (int)r : -1, lane);
+    if (ok && lane == 0) y[r] = b;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dense_gemv(int64_t n, const double* __restrict__ X,
+                                                    const double* __restrict__ y,
+                                                    double* __restrict__ x, double* __restrict__ out,
+                                                    const int* __restrict__ perm, Ctl c) {
+  if (inactive(c)) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double* row = X + r * n;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t q = lane;
+    for (; q + 32 < n; q += 64) {
+      s0 = fma(__ldcs(&row[q]), __ldg(&y[q]), s0);
+      s1 = fma(__ldcs(&row[q + 32]), __ldg(&y[q + 32]), s1);
+    }
+    if (q < n) s0 = fma(__ldcs(&row[q]), __ldg(&y[q]), s0);
+    const double z = warp_sum(s0 + s1);
+    if (lane == 0) {
+      x[r] = z;
+      if (out) out[perm ? perm[r] : r] = z;
+    }
+  }
+}
+
 // corr = S_i s, sum(corr) -> mu2 (bd/precond.py:308-311: `correction[:nh] =
 // stiff_intra @ s` then its mean inside _bulk_inverse).
 template <int G>
