@@ -46,3 +46,20 @@ def test_tile_kernel_matches_oracle(problems, name, kernel, inbox, monkeypatch, 
         y = rng.standard_normal(g.shape[0])
         got, want = ic.apply_inverse(y), ref.apply(y)
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("dense_max", ["0", "100000"])
+@pytest.mark.parametrize("name", ["slab", "torso"])
+def test_exact_inner_paths_match_oracle(problems, name, dense_max, monkeypatch, rng):
+    """The exact inner as supernodal passes (BD_EXACT_DENSE_MAX=0: split
+    external phases, panel inverses) and as the dense explicit inverse both
+    give the oracle's exact solve (1e-10 relative)."""
+    monkeypatch.setenv("BD_EXACT_DENSE_MAX", dense_max)
+    g, _, _ = problems[name]
+    ref = orc.make_inner("exact", g)
+    ex = bd.ExactFactorization()
+    ex.setup(g)
+    for _ in range(2):
+        y = rng.standard_normal(g.shape[0])
+        got, want = ex.apply_inverse(y), ref.apply(y)
+        assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max()
