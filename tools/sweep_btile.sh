@@ -1,4 +1,4 @@
-# dev: 5x5x5 lattice tiles (128-row rtile, smem inverse) vs the 4x4x4 default
-BD_DEBUG=1 MODES=btile python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply|auto|btile n=|launch"
-BD_BTILE_ROWS=125 BD_DEBUG=1 MODES=btile python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply|auto|btile n=|launch|rel diff"
-BD_BTILE_ROWS=125 BD_DEBUG=1 MODES=btile python tools/trsv_bench.py 256,256,128 10 2>&1 | grep -E "us per apply|btile n=|launch"
+# dev sweep: blocked-tile triangular-solve kernels (BD_BTILE_KERNEL) on the
+# cfg2 slab and at cfg3 size (forward + backward pair, median of N reps)
+MODES=btile@auto,btile@reg,btile@rsmem,btile@smem python tools/trsv_bench.py 128,128,64 30 2>&1 | grep -E "us per apply|rel diff"
+MODES=btile@auto,btile@rsmem,btile@smem python tools/trsv_bench.py 256,256,128 10 2>&1 | grep -E "us per apply|rel diff"
