@@ -408,6 +408,20 @@ def run_sharded(args, rank, world, local_rank):
     n, m = wl.n, wl.n_heart
     base_dof = 2 * (129 * 129 * 65)
     steps_s = args.steps / (ms / 1e3)
+    # per-GPU HBM GB/s (BASELINE config 3): this rank's algorithmic bytes per
+    # PCG iteration (SURVEY §8d on the local blocks and block-Jacobi factors)
+    # over the measured time per iteration, reported as the minimum over ranks
+    lp = sim.lp
+    try:
+        nnz_l1 = int(sim.prec.bulk.factor_info()["nnz"])
+        nnz_lk = int(sim.prec.schur.factor_info()["nnz"])
+    except Exception:  # non-factor inners (jacobi)
+        nnz_l1 = nnz_lk = 0
+    b_loc = iteration_bytes(lp.n_own, lp.m_own, lp.S1.nnz, lp.Si.nnz, nnz_l1, nnz_lk)
+    it_total = max(1.0, float(np.sum(iters)))
+    gbs = torch.tensor([b_loc / (ms / it_total * 1e-3) / 1e9], device=dev, dtype=torch.float64)
+    dist.all_reduce(gbs, op=dist.ReduceOp.MIN)
+    gbs_min = float(gbs.item())
     value = steps_s * (n + m) / base_dof  # cfg2-equivalent time steps per second (aggregate)
     if rank == 0:
         emit(({
@@ -420,6 +434,11 @@ def run_sharded(args, rank, world, local_rank):
                        "dof": n + m, "raw_steps_per_s": round(steps_s, 4),
                        "value_definition": "steps/s x dof / dof(cfg2): cfg2-equivalent steps/s",
                        "pcg_iters_per_step": round(float(np.mean(iters)), 2),
+                       "ms_per_pcg_iter": round(ms / it_total, 4),
+                       "hbm_gbs_per_gpu": round(gbs_min, 1),
+                       "hbm_gbs_definition": "algorithmic bytes per PCG iteration of the rank's "
+                                             "blocks (SURVEY 8d) / time per iteration, min over "
+                                             "ranks",
                        "pcg_loop": "cuda graph" if graph_used else f"eager ({graph_err})",
                        "parallelism": f"mesh partition x{world}"},
             "gpu_launches": int(ctx.launches() - launches0), "clocks": clk,
