@@ -152,9 +152,13 @@ class Comm:
         self.dist = dist
         self.device = device
         self._idx = {}
+        # one rank: every sum is already global (no collective in the loop)
+        self.single = dist.get_world_size() == 1
 
     def allreduce(self, vals):
         """Host list -> host list (setup only: synchronises)."""
+        if self.single:
+            return [float(v) for v in vals]
         torch = _torch()
         t = torch.tensor(vals, dtype=torch.float64, device=self.device)
         self.dist.all_reduce(t)
@@ -162,7 +166,8 @@ class Comm:
 
     def allreduce_(self, t):
         """In-place global sum of a device tensor (no host round trip)."""
-        self.dist.all_reduce(t)
+        if not self.single:
+            self.dist.all_reduce(t)
         return t
 
     def _index(self, key, idx):
@@ -289,18 +294,20 @@ class DistributedBlockLU:
         self.p1 = self.pk = self.si = 0
         self._corr = None  # pad(S_i s): torso rows stay zero, heart rows rewritten per apply
 
-    def bulk_inverse(self, y):
+    def bulk_inverse(self, y, mean=None):
+        """`mean` (device 0-d): mean(y) when the caller already reduced it."""
         self.p1 += 1
         s = self.s
-        mean = s.mean_u_t(y)
+        if mean is None:
+            mean = s.mean_u_t(y)
         z = s.be.inner_apply(self.bulk, y - mean)
         z = z - s.mean_u_t(z)
         return z + mean / self.beta
 
-    def apply(self, r):
+    def apply(self, r, mean_ru=None):
         s, lp = self.s, self.s.lp
         ru, rv = r[: lp.n_own], r[lp.n_own:]
-        t = self.bulk_inverse(ru)
+        t = self.bulk_inverse(ru, mean_ru)
         tg = s.heart_ghosts(t[: lp.m_own])  # collective on all ranks
         self.si += 1
         self.pk += 1
@@ -349,8 +356,8 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
         st["converged"] = True
         return dsys.normalize(x), st
 
-    def precond(r):
-        z = prec.apply(r)
+    def precond(r, mean_ru=None):
+        z = prec.apply(r, mean_ru)
         z[:n] -= dsys.mean_u_t(z[:n])  # _deflate
         return z
 
@@ -381,11 +388,14 @@ def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e
         S["x"].addcmul_(d, alpha)
         S["r"].addcmul_(q, alpha, value=-1.0)
         S["iters"].add_(go.to(torch.int64))
-        relk = torch.sqrt(dsys.dot_t(S["r"], S["r"])) / nb
+        # ‖r‖² and Σ r_u (the first bulk solve's mean) in one all-reduce
+        pair = torch.stack([torch.dot(S["r"], S["r"]), S["r"][:n].sum()])
+        dsys.comm.allreduce_(pair)
+        relk = torch.sqrt(pair[0]) / nb
         S["k"].add_(1)
         S["res"].index_put_((S["k"],), torch.where(go, relk, torch.full_like(relk, -1.0)))
         act = go & ~(relk <= tol)
-        zz = precond(S["r"])
+        zz = precond(S["r"], pair[1] / dsys.lp.n_global)
         rho_next = dsys.dot_t(S["r"], zz)
         S["pre"].index_put_((S["k"],), torch.where(act, rho_next, torch.full_like(rho_next, float("nan"))))
         beta = torch.where(act, rho_next / rho, zero)
