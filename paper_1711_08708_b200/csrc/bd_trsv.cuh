@@ -1152,7 +1152,7 @@ __host__ __device__ constexpr size_t rt_smem(int xs, int es, int rps, int is) {
 // preparation is a single round of independent loads; with bt_next set the
 // pass also writes its output into the next pass's tile order through opos.
 template <bool kSmemInv, bool kTileRhs, class Rhs>
-__global__ void __launch_bounds__(256, kSmemInv ? 6 : 4)
+__global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
     k_trsv_rtile(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
                  const double* __restrict__ bt, const int* __restrict__ opos,
                  double* __restrict__ bt_next) {
