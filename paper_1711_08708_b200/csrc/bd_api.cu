@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <future>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -287,6 +288,13 @@ bd_status fail(bd_ctx* ctx, bd_status st, const std::string& msg) {
 template <class T>
 cudaError_t dalloc(T** p, int64_t count) {
   return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1));
+}
+
+static double wall_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static void setup_log(const char* what, double t0) {
+  if (getenv("BD_DEBUG")) std::fprintf(stderr, "[bd] setup %s %.2f s\n", what, wall_s() - t0);
 }
 
 int grid_for(bd_ctx* ctx, int64_t items, int per_block) {
@@ -944,6 +952,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   const int64_t is = dev::bt_even(rs * (rs + 1) / 2);
   const int rps = dev::bt_round8(rs + 1);
   int emax = 0;
+#pragma omp parallel for reduction(max : emax) schedule(static)
   for (int t = 0; t < nt; ++t) {
     int cnt = 0;
     for (int64_t k = bs.tile_row_ptr[t]; k < bs.tile_row_ptr[t + 1]; ++k)
@@ -956,6 +965,8 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   std::vector<int32_t> nr(nt), row((size_t)nt * rs, -1), in((size_t)nt * xs, -1);
   std::vector<uint16_t> rp((size_t)nt * rps, 0), slot((size_t)nt * es, 0);
   std::vector<double> val((size_t)nt * es, 0.0), inv((size_t)nt * is, 0.0);
+  // tiles fill disjoint ranges: host threads
+#pragma omp parallel for schedule(dynamic, 64)
   for (int t = 0; t < nt; ++t) {
     const int r0 = bs.tile_row_ptr[t], n_ = bs.tile_row_ptr[t + 1] - r0;
     nr[t] = n_;
@@ -1095,6 +1106,7 @@ void free_btile(DevBTile* d) {
 bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
                       const double* coords, int dim) {
   bd_ctx* ctx = p->ctx;
+  const double t_s = wall_s();
   const int target = getenv("BD_BTILE_ROWS") ? atoi(getenv("BD_BTILE_ROWS")) : 64;
   const char* part = getenv("BD_TILE_PART");  // "grid" (default) | "rcb"
   const bool grid = !(part && std::string(part) == "rcb");
@@ -1129,6 +1141,7 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
     partition_coords(lower.n, dim, coords, ntiles, &tile);
   else
     partition_rows(lower, ntiles, &tile);
+  setup_log("tiles", t_s);
   int E = 4;
   for (int64_t i = 0; i < lower.n; ++i)
     while (E < lower.indptr[i + 1] - lower.indptr[i] - 1) E <<= 1;
@@ -1137,15 +1150,26 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   DTileSchedule dl, du;
   BTileSchedule bl, bu;
   std::string why;
-  bool ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
-            build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+  // forward and backward schedules are independent: build them concurrently
+  auto build_pair = [&](const std::vector<int32_t>& tl, int nt) {
+    std::string why_u;
+    auto fu = std::async(std::launch::async, [&] {
+      return build_dtile_schedule(upper, false, tl, nt, E, &du, &why_u);
+    });
+    const bool okl = build_dtile_schedule(lower, true, tl, nt, E, &dl, &why);
+    const bool oku = fu.get();
+    if (okl && !oku) why = why_u;
+    return okl && oku;
+  };
+  bool ok = build_pair(tile, ntiles);
   if (!ok && coords && dim > 0 && grid) {  // e.g. a cyclic tile graph: fall back to RCB tiles
     ntiles = (int)std::max<int64_t>(1, lower.n / target);
     partition_coords(lower.n, dim, coords, ntiles, &tile);
-    ok = build_dtile_schedule(lower, true, tile, ntiles, E, &dl, &why) &&
-         build_dtile_schedule(upper, false, tile, ntiles, E, &du, &why);
+    ok = build_pair(tile, ntiles);
   }
+  setup_log("dtile schedules", t_s);
   ok = ok && build_btile_schedule(dl, &bl, &why) && build_btile_schedule(du, &bu, &why);
+  setup_log("btile schedules", t_s);
   if (ok && (std::max(bl.tmax, bu.tmax) > 256 || std::max(bl.Ex, bu.Ex) > 16 ||
              (std::max(bl.Ex, bu.Ex) > 8 && std::max(bl.tmax, bu.tmax) > dev::RT_ROWS) ||
              std::max(bl.xmax, bu.xmax) > 512 ||
@@ -1160,6 +1184,7 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   if (!ok) return BD_OK;
   TRY(upload_btile(ctx, bl, &p->BL));
   TRY(upload_btile(ctx, bu, &p->BU));
+  setup_log("btile upload", t_s);
   // inbox mode (BD_BTILE_INBOX=1; measured 1.5% slower than polling the output
   // vector): per pass, the inbox slots (consumer tile, input slot)
   // fed by each row
@@ -2097,7 +2122,9 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   std::string msg;
   HostCsr lower;
   if (kind == BD_INNER_IC0) {
+    const double t_f = wall_s();
     const int rc = ic0_factor(a, max_restarts, &lower, &p->restarts, &msg);
+    setup_log("ic0 factor", t_f);
     if (rc != 0) {
       bd_inner_destroy(p);
       return fail(ctx, BD_EPRECOND, msg);
