@@ -12,6 +12,7 @@ S_i SpMVs and the mean projections fused into their producers.
 from __future__ import annotations
 
 import ctypes as C
+from concurrent.futures import ThreadPoolExecutor
 from abc import ABC, abstractmethod
 from dataclasses import dataclass
 
@@ -237,17 +238,31 @@ class BlockLUPreconditioner:
         self.inner_name = inner
         self.regularized = regularize_stiffness(system.stiff_total)
         coords = _coords(system)
+        # the two inner factorisations are independent host work (the C setup
+        # releases the GIL): the bulk one runs on a worker thread while the
+        # Schur block is built and factored here; a bulk error still wins
         self.inner_bulk = make_inner(inner)
-        self.inner_bulk.setup(self.regularized.grounded(), coords=coords)
-        if monodomain_matrix is None:
-            if system.mesh is None or system.params is None:
-                raise PreconditionerError("system carries no mesh/params; pass monodomain_matrix")
-            monodomain_matrix = build_monodomain_matrix(system.mesh, system.params, system.gamma,
-                                                        getattr(system, "fibers", None))
+        grounded = self.regularized.grounded()
+        _lib.Context.default()  # one shared context, created here before the worker starts
+        with ThreadPoolExecutor(max_workers=1) as pool:
+            bulk = pool.submit(self.inner_bulk.setup, grounded, coords=coords)
+            schur_err = None
+            try:
+                if monodomain_matrix is None:
+                    if system.mesh is None or system.params is None:
+                        raise PreconditionerError(
+                            "system carries no mesh/params; pass monodomain_matrix")
+                    monodomain_matrix = build_monodomain_matrix(
+                        system.mesh, system.params, system.gamma, getattr(system, "fibers", None))
+                self.inner_schur = make_inner(inner)
+                self.inner_schur.setup(monodomain_matrix,
+                                       coords=None if coords is None else coords[: system.n_heart])
+            except Exception as exc:  # reported after the bulk result
+                schur_err = exc
+            bulk.result()
+            if schur_err is not None:
+                raise schur_err
         self.monodomain_matrix = monodomain_matrix
-        self.inner_schur = make_inner(inner)
-        self.inner_schur.setup(monodomain_matrix,
-                               coords=None if coords is None else coords[: system.n_heart])
         nat = system.native
         h = C.c_void_p()
         _lib.check(_lib.lib().bd_blocklu_create(nat.handle, self.inner_bulk.handle,
