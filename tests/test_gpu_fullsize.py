@@ -36,7 +36,7 @@ def run():
     pre = bd.BlockLUPreconditioner(sysm, inner="ic0", monodomain_matrix=km)
     state = bd.SimState.resting(sysm.n, sysm.n_heart, wl.ionic)
     pts = wl.mesh.vertices[: sysm.n_heart]
-    steps = min(len(ref["iters"]), 5)
+    steps = min(len(ref["iters"]), int(os.environ.get("BD_FULLSIZE_STEPS", "5")))
     out = {"iters": [], "trace": [], "u": [], "v": []}
     for k in range(steps):
         state, st = bd.time_step(state, sysm, pre, wl.ionic, wl.protocol, wl.dt, tol=wl.tol,
