@@ -209,6 +209,16 @@ typedef struct bd_asm bd_asm;
 bd_status bd_assemble_p1(bd_ctx* ctx, int dim, int64_t nv, const double* vertices, int64_t ne,
                          const int64_t* elements, const double* sigma, const double* sigma2,
                          bd_asm** out, int64_t* nnz);
+/* Heart conductivity tensors of the transmural-rotation fibre model on the
+ * device (3D; centroid, fibre angle linear in z, frame (f, s, e_z)):
+ * model = {z0, z1, angle0_deg, angle1_deg}; gi / ge = the three intra / extra
+ * gains (fibre, sheet, normal; orthotropic != 0) or (longitudinal,
+ * transverse, -) for the transversely isotropic form.  Host in, host out
+ * (ne x 3 x 3 each). */
+bd_status bd_tensors_transmural(bd_ctx* ctx, int64_t nv, const double* vertices, int64_t ne,
+                                const int64_t* elements, const double* model, const double* gi,
+                                const double* ge, int orthotropic, double* out_intra,
+                                double* out_extra);
 /* Copy the result to host arrays (indptr nv+1, indices nnz, data nnz,
  * mass nv); any pointer may be NULL. */
 bd_status bd_assemble_export(bd_asm* a, int64_t* indptr, int32_t* indices, double* data,

@@ -85,6 +85,7 @@ SIGNATURES = [
     ("bd_membrane_gate", _i32, [_vp, _i64, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _dbl, _vp]),
     ("bd_assemble_p1", _i32, [_vp, C.c_int, _i64, _vp, _i64, _vp, _vp, _vp, _pp, C.POINTER(_i64)]),
     ("bd_assemble_export", _i32, [_vp, _vp, _vp, _vp, _vp]),
+    ("bd_tensors_transmural", _i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     ("bd_assemble_destroy", _i32, [_vp]),
     ("bd_step_track", _i32, [_vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, C.POINTER(_dbl)]),
 ]

@@ -115,12 +115,38 @@ class DeviceAssembler:
         self.verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
         self.el = np.ascontiguousarray(mesh.elements, dtype=np.int64)
         self.el_h = np.ascontiguousarray(self.el[self.heart])
-        tf = TensorField(field_params, d, "bar1", fibers)
-        cent = self.verts[self.el_h].mean(axis=1)
-        self.intra, self.extra = (np.ascontiguousarray(a, dtype=np.float64)
-                                  for a in tf._heart_tensors(cent))
+        self.intra, self.extra = self._heart_tensors(field_params, fibers)
         self.params = field_params
         self._mass = {}
+
+    def _heart_tensors(self, p, fibers):
+        """(σ_i, σ_e) per heart element: on the device for the transmural
+        rotation of configs 2/3 (`bd_tensors_transmural`), else the host
+        TensorField evaluation."""
+        from .conductivity import TransmuralRotation
+
+        d = self.mesh.dim
+        if isinstance(fibers, TransmuralRotation) and d == 3:
+            import ctypes as C
+            L = self._lib
+            ne = self.el_h.shape[0]
+            oi = np.empty((ne, 3, 3))
+            oe = np.empty((ne, 3, 3))
+            if p.orthotropic:
+                gi = [p.g_i_l, p.g_i_t, p.g_i_n if p.g_i_n is not None else p.g_i_t]
+                ge = [p.g_e_l, p.g_e_t, p.g_e_n if p.g_e_n is not None else p.g_e_t]
+            else:
+                gi, ge = [p.g_i_l, p.g_i_t, 0.0], [p.g_e_l, p.g_e_t, 0.0]
+            arr = lambda v: (C.c_double * len(v))(*[float(x) for x in v])  # noqa: E731
+            model = arr([fibers.z0, fibers.z1, fibers.angle0, fibers.angle1])
+            L.check(L.lib().bd_tensors_transmural(
+                self.ctx.handle, self.verts.shape[0], self.verts.ctypes.data, ne,
+                self.el_h.ctypes.data, model, arr(gi), arr(ge), int(bool(p.orthotropic)),
+                oi.ctypes.data, oe.ctypes.data), self.ctx.handle)
+            return oi, oe
+        tf = TensorField(p, d, "bar1", fibers)
+        cent = self.verts[self.el_h].mean(axis=1)
+        return tuple(np.ascontiguousarray(a, dtype=np.float64) for a in tf._heart_tensors(cent))
 
     def _torso(self, base: np.ndarray) -> np.ndarray:
         """Full-element tensor array: heart rows from `base`, torso c·I."""

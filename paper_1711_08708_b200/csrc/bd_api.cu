@@ -2810,6 +2810,34 @@ bd_status bd_assemble_p1(bd_ctx* ctx, int dim, int64_t nv, const double* vertice
   return BD_OK;
 }
 
+bd_status bd_tensors_transmural(bd_ctx* ctx, int64_t nv, const double* vertices, int64_t ne,
+                                const int64_t* elements, const double* model, const double* gi,
+                                const double* ge, int orthotropic, double* out_intra,
+                                double* out_extra) {
+  if (!ctx || !vertices || !model || !gi || !ge || !out_intra || !out_extra || ne < 0 || nv <= 0 ||
+      (ne > 0 && !elements))
+    return fail(ctx, BD_EINVAL, "bd_tensors_transmural: bad arguments");
+  Scope sc(ctx);
+  cudaStream_t st = ctx->stream;
+  asmk::DevScratch S;
+  double *xv, *oi, *oe;
+  int64_t* el;
+  if (S.get(&xv, nv * 3) || S.get(&el, ne * 4) || S.get(&oi, ne * 9) || S.get(&oe, ne * 9))
+    return fail(ctx, BD_ECUDA, "bd_tensors_transmural: allocation failed");
+  CK(ctx, cudaMemcpyAsync(xv, vertices, sizeof(double) * nv * 3, cudaMemcpyHostToDevice, st));
+  if (ne > 0) {
+    CK(ctx, cudaMemcpyAsync(el, elements, sizeof(int64_t) * ne * 4, cudaMemcpyHostToDevice, st));
+    asmk::k_tensors_transmural<<<grid_for(ctx, ne, 256), 256, 0, st>>>(
+        ne, xv, el, model[0], model[1], model[2], model[3], gi[0], gi[1], gi[2], ge[0], ge[1], ge[2],
+        orthotropic, oi, oe);
+    LAUNCHED(ctx);
+    CK(ctx, cudaMemcpyAsync(out_intra, oi, sizeof(double) * ne * 9, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(out_extra, oe, sizeof(double) * ne * 9, cudaMemcpyDeviceToHost, st));
+  }
+  CK(ctx, cudaStreamSynchronize(st));
+  return BD_OK;
+}
+
 bd_status bd_assemble_export(bd_asm* a, int64_t* indptr, int32_t* indices, double* data,
                              double* mass) {
   if (!a) return BD_EINVAL;

@@ -220,6 +220,50 @@ __global__ void __launch_bounds__(256) k_rowptr(int64_t nv, int64_t nnz,
   }
 }
 
+// Heart tensors of the transmural-rotation fibre model (configs 2/3,
+// conductivity.py TransmuralRotation + TensorField._heart_tensors) per
+// element on the device: centroid, fibre angle linear in z, frame
+// (f, s, n) = ((c, s, 0), (-s, c, 0), e_z), and sigma = sum_k g_k e_k e_k^T
+// (orthotropic) or g_l f f^T + g_t (I - f f^T) (transversely isotropic),
+// in the host's term order.
+__global__ void __launch_bounds__(256) k_tensors_transmural(
+    int64_t ne, const double* __restrict__ xv, const int64_t* __restrict__ el, double z0,
+    double z1, double a0, double a1, double gi0, double gi1, double gi2, double ge0, double ge1,
+    double ge2, int ortho, double* __restrict__ out_i, double* __restrict__ out_e) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double cz = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) cz += xv[el[e * 4 + a] * 3 + 2];
+    cz /= 4.0;
+    double z = (cz - z0) / (z1 - z0);
+    z = z < 0.0 ? 0.0 : (z > 1.0 ? 1.0 : z);
+    const double th = (a0 + (a1 - a0) * z) * (3.141592653589793 / 180.0);
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double fr[3][3] = {{cs, sn, 0.0}, {-sn, cs, 0.0}, {0.0, 0.0, 1.0}};
+    for (int w = 0; w < 2; ++w) {
+      const double g0 = w ? ge0 : gi0, g1 = w ? ge1 : gi1, g2 = w ? ge2 : gi2;
+      double* o = (w ? out_e : out_i) + e * 9;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double v;
+          if (ortho) {  // sum_k g_k (e_k e_k^T), no contraction (numpy order)
+            v = __dadd_rn(0.0, __dmul_rn(g0, __dmul_rn(fr[0][r], fr[0][q])));
+            v = __dadd_rn(v, __dmul_rn(g1, __dmul_rn(fr[1][r], fr[1][q])));
+            v = __dadd_rn(v, __dmul_rn(g2, __dmul_rn(fr[2][r], fr[2][q])));
+          } else {
+            const double pr = __dmul_rn(fr[0][r], fr[0][q]);
+            v = __dadd_rn(__dmul_rn(g0, pr), __dmul_rn(g1, __dsub_rn(r == q ? 1.0 : 0.0, pr)));
+          }
+          o[r * 3 + q] = v;
+        }
+    }
+  }
+}
+
 // host: device scratch buffers freed when the owner goes out of scope
 struct DevScratch {
   std::vector<void*> p;

@@ -91,3 +91,16 @@ def test_time_step_on_device_assembled_system():
     rel = np.sqrt(np.sum((ud - uh) ** 2) + np.sum((vd - vh) ** 2)) / np.sqrt(
         np.sum(uh ** 2) + np.sum(vh ** 2))
     assert rel <= 1e-8
+
+
+@pytest.mark.parametrize("ortho", [True, False])
+def test_transmural_tensors_on_device(ortho):
+    """Heart tensors of the transmural-rotation model evaluated on the device
+    (bd_tensors_transmural) vs the host TensorField (cos/sin to the last ulps)."""
+    wl = configs.cfg2((6, 6, 4))
+    params = wl.params if ortho else default_params(3)
+    da = DeviceAssembler(wl.mesh, params, wl.fibers)
+    tf = TensorField(params, 3, "bar1", wl.fibers)
+    hi, he = tf._heart_tensors(wl.mesh.vertices[da.el_h].mean(axis=1))
+    for dev, host in ((da.intra, hi), (da.extra, he)):
+        assert np.abs(dev - host).max() <= 1e-14 * np.abs(host).max()
