@@ -2142,7 +2142,7 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   p->G = pick_g(avg - 1.0);
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
-  const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 8192;
+  const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 16384;
   if (st == BD_OK && kind == BD_INNER_EXACT && n <= dense_max) {
     // explicit inverse of P A P^T from the sparse factor, one column per host
     // thread (X^T = X up to rounding; row j of X holds the solve with e_j)
