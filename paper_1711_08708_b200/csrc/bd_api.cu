@@ -178,6 +178,7 @@ struct DevSuper {
   int* sn_start = nullptr;
   int* sn_size = nullptr;
   int* task_sn = nullptr;
+  int* task_w = nullptr;  // lanes per small supernode of each task (nullptr: 32)
   int ntasks = 0;
   int grid = 0;
 };
@@ -616,7 +617,18 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
   auto order = [&](const std::vector<int32_t>& lv, DevSuper* out, bool split) -> bd_status {
     std::vector<int32_t> idx(ns);
     std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return lv[a] < lv[b]; });
+    // lanes per small supernode: one warp each by default; BD_SUPER_PACK=1
+    // packs 32/W of them per warp, W the next power of two >= the size (at
+    // least 4) -- measured neutral-to-slower on cfg1 (18.3 vs 17.9 ms/step)
+    const bool pack = getenv("BD_SUPER_PACK") && atoi(getenv("BD_SUPER_PACK")) != 0;
+    auto lanes = [&](int32_t s) -> int {
+      if (!pack || size[s] > 16) return 32;
+      return size[s] > 8 ? 16 : size[s] > 4 ? 8 : 4;
+    };
+    // level order; within a level, small supernodes grouped by lane width
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+      return lv[a] != lv[b] ? lv[a] < lv[b] : lanes(a) < lanes(b);
+    });
     std::vector<int32_t> st(ns), sz(ns), tasks;
     for (int64_t k = 0; k < ns; ++k) {
       st[k] = start[idx[k]];
@@ -628,8 +640,8 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
     // subtree) gets its external phase split into SN_CHUNK-row chunk tasks
     // placed right before it, so many CTAs stream it; the supernode's own task
     // then waits for its chunks and does the dense phase.
-    std::vector<int32_t> kind, arg;
-    bool any_split = false;
+    std::vector<int32_t> kind, arg, tw;
+    bool any_split = false, any_pack = false;
     for (int64_t k = 0; k < ns;) {
       if (sz[k] > 32) {
         if (split && ext[idx[k]] >= split_min) {
@@ -648,14 +660,21 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
           kind.push_back(0);
           arg.push_back(0);
         }
+        tw.resize(tasks.size(), 32);
         ++k;
         continue;
       }
+      // up to 16 warps x 32/W supernodes of one level and lane width W
+      const int W = lanes(idx[k]);
       tasks.push_back((int32_t)k);
       kind.push_back(0);
       arg.push_back(0);
+      tw.push_back(W);
+      any_pack |= W < 32;
       int64_t e = k + 1;
-      while (e < ns && e - k < 16 && sz[e] <= 32 && lv[idx[e]] == lv[idx[k]]) ++e;
+      while (e < ns && e - k < 16 * (32 / W) && sz[e] <= 32 && lv[idx[e]] == lv[idx[k]] &&
+             lanes(idx[e]) == W)
+        ++e;
       k = e;
     }
     tasks.push_back((int32_t)ns);
@@ -697,6 +716,7 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
     CK(ctx, upload_vec(&out->sn_start, st));
     CK(ctx, upload_vec(&out->sn_size, sz));
     CK(ctx, upload_vec(&out->task_sn, tasks));
+    if (any_pack) CK(ctx, upload_vec(&out->task_w, tw));
     if (any_split) {
       CK(ctx, upload_vec(&out->task_kind, kind));
       CK(ctx, upload_vec(&out->task_arg, arg));
@@ -738,6 +758,7 @@ void free_super(DevSuper* s) {
   cudaFree(s->sn_start);
   cudaFree(s->sn_size);
   cudaFree(s->task_sn);
+  cudaFree(s->task_w);
 }
 
 bd_status upload_cluster(bd_ctx* ctx, const ClusterSchedule& cs, DevCluster* out) {
@@ -1429,7 +1450,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tl{(int)p->n,        p->L.rowptr,  p->L.col,    p->L.val, p->SL.sn_start,
                      p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr,
                      p->SL.task_kind,   p->SL.task_arg, p->SL.sn_cnt, p->rext,
-                     p->SL.pinv,        p->SL.sn_pan};
+                     p->SL.pinv,        p->SL.sn_pan,  p->SL.task_w};
     dev::k_trsv_super<true, Rhs><<<p->SL.grid, 512, 0, st>>>(tl, rhs, p->y_int, nullptr, c, ctr0,
                                                               ctr0 + 1);
     LAUNCHED(ctx);
@@ -1438,7 +1459,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
                      p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm,
                      nullptr,           nullptr,        nullptr,      nullptr,
-                     p->SU.pinv,        p->SU.sn_pan};
+                     p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w};
     dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
         tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
     LAUNCHED(ctx);

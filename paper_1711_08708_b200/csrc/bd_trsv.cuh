@@ -1744,6 +1744,7 @@ struct SuperTri {
   // supernode's first panel at sn_pan[supernode]
   const double* pinv;
   const int* sn_pan;
+  const int* task_w;  // small-supernode tasks: lanes per supernode (nullable: 32)
 };
 
 constexpr int SN_MAX = 1024;
@@ -1751,11 +1752,13 @@ constexpr int SN_CHUNK = 64;  // rows per external-phase chunk (16 warps x RW 4)
 
 // One warp solves one small supernode (<= 32 rows): external dots RW rows at
 // a time, then the dense triangle with the coefficients in registers.
+// W: lanes per supernode (4, 8, 16 or 32; 32/W supernodes share a warp, all
+// lanes take part in the shuffles, ns = 0 marks an idle group).
 template <bool LOWER, class Rhs>
 __device__ __forceinline__ void super_small_warp(const SuperTri& t, const Rhs& rhs,
                                                  double* __restrict__ x,
                                                  double* __restrict__ out, int c0, int ns,
-                                                 int lane) {
+                                                 int lane, int W = 32) {
   const int c1 = c0 + ns;
   // lane l owns the l-th row in solve order: its right-hand side minus its
   // external part, entries walked sequentially, 4 loads in flight
@@ -1814,19 +1817,24 @@ __device__ __forceinline__ void super_small_warp(const SuperTri& t, const Rhs& r
   double win[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) win[u] = coef(u);
-  for (int j0 = 0; j0 < ns; j0 += 8) {
+  // loop bound uniform over the warp (W); groups with fewer rows idle through
+  // the tail (the shuffles need every lane)
+  const int nsw = __reduce_max_sync(0xffffffffu, ns);
+  for (int j0 = 0; j0 < nsw; j0 += 8) {
     double nxt[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) nxt[u] = coef(j0 + 8 + u);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int jj = j0 + u;
-      if (jj >= ns) break;
-      const double rj = __shfl_sync(0xffffffffu, ri, jj);
-      const double dj = __shfl_sync(0xffffffffu, diag, jj);
-      const double xj = __ddiv_rn(rj, dj);
-      if (lane == jj) ri = xj;
-      if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(win[u], xj));
+      if (jj >= nsw) break;
+      const double rj = __shfl_sync(0xffffffffu, ri, jj, W);
+      const double dj = __shfl_sync(0xffffffffu, diag, jj, W);
+      if (jj < ns) {
+        const double xj = __ddiv_rn(rj, dj);
+        if (lane == jj) ri = xj;
+        if (ok && lane > jj) ri = __dsub_rn(ri, __dmul_rn(win[u], xj));
+      }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) win[u] = nxt[u];
@@ -1928,9 +1936,14 @@ __global__ void __launch_bounds__(512, 2) k_trsv_super(SuperTri t, Rhs rhs, doub
     unsigned long long* trace = ((g_tile_trace_steps < 0) == LOWER) ? g_tile_trace : nullptr;
     if (trace && threadIdx.x == 0) t_beg = gtimer();
     if (s1 - s0 > 1 || t.sn_size[s0] <= 32) {
-      // group of small independent supernodes: one warp each, no CTA barrier
-      if (s0 + warp < s1)
-        super_small_warp<LOWER>(t, rhs, x, out, t.sn_start[s0 + warp], t.sn_size[s0 + warp], lane);
+      // group of small independent supernodes: W lanes each (32/W per warp),
+      // no CTA barrier
+      const int W = t.task_w ? t.task_w[task] : 32;
+      const int sidx = s0 + warp * (32 / W) + lane / W;
+      const bool has = sidx < s1;
+      if (warp * (32 / W) < s1 - s0)
+        super_small_warp<LOWER>(t, rhs, x, out, has ? t.sn_start[sidx] : 0,
+                                has ? t.sn_size[sidx] : 0, lane % W, W);
       if (trace) {
         __syncthreads();
         if (threadIdx.x == 0 && task < tsteps) {
