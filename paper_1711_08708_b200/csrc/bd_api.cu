@@ -198,6 +198,7 @@ struct bd_inner {
   bool btile = false;
   DevBTile BL, BU;
   double* rtmp = nullptr;
+  double* rhs_pre = nullptr;  // btile: pre-evaluated non-scalar right-hand side
   double* rext = nullptr;  // supernodal forward: precomputed external phases (n)
   double* dense = nullptr; // exact inner, small n: explicit inverse (P A P^T)^{-1}, row-major
   // tiled cooperative schedule (IC(0) factors with short rows)
@@ -1262,6 +1263,11 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
     p->BL.pipe = p->BU.pipe = false;
     p->BL.tile_rhs = p->BU.tile_rhs = false;
   }
+  // BD_RHS_PRE=1: heavy right-hand sides (the Schur solve's r_v - S_i t)
+  // evaluated by one streaming kernel before the forward pass instead of
+  // inside its tiles; measured 0.5-1 % slower at cfg2, so off by default
+  if (getenv("BD_RHS_PRE") && atoi(getenv("BD_RHS_PRE")) != 0)
+    if (dalloc(&p->rhs_pre, lower.n)) return fail(ctx, BD_ECUDA, "btile: out of device memory");
   p->btile = true;
   return BD_OK;
 }
@@ -1397,10 +1403,19 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     const bool ib = p->BL.inbox != nullptr;
     const int64_t nf1 = ib ? (int64_t)p->BL.ntiles * p->BL.xs : p->n;
     const int64_t nf2 = ib ? (int64_t)p->BU.ntiles * p->BU.xs : p->n;
+    if (!Rhs::kScalar && p->rhs_pre) {
+      dev::k_rhs_eval<G, Rhs><<<grid_for(ctx, p->n, dev::TPB / G), dev::TPB, 0, st>>>(
+          (int)p->n, rhs, p->rhs_pre, c);
+      LAUNCHED(ctx);
+    }
     dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
                                                                   dev::SENTINEL, c);
     LAUNCHED(ctx);
-    TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr));
+    if (!Rhs::kScalar && p->rhs_pre)
+      TRY(launch_btile(p, p->BL, dev::RhsVec{p->rhs_pre, (int)p->n, nullptr, nullptr}, p->y_int, c,
+                       ctr0, ctr0 + 1, nullptr));
+    else
+      TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr));
     dev::k_fill<<<grid_for(ctx, nf2, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : xg, nf2,
                                                                   dev::SENTINEL, c);
     LAUNCHED(ctx);
@@ -2278,6 +2293,7 @@ bd_status bd_inner_destroy(bd_inner* p) {
   free_btile(&p->BU);
 
   cudaFree(p->rtmp);
+  cudaFree(p->rhs_pre);
   cudaFree(p->rext);
   cudaFree(p->dense);
   cudaFree(p->perm);
