@@ -609,13 +609,21 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
   for (int64_t sn = 0; sn < ns; ++sn)
     for (int64_t i = start[sn]; i < start[sn] + size[sn]; ++i)
       ext[sn] += L.indptr[i + 1] - L.indptr[i] - 1 - (i - start[sn]);
+  // backward (U = L^T): the external entries of row j are L's entries (i, j)
+  // below j's supernode
+  std::vector<int64_t> extb(ns, 0);
+  for (int64_t sn = 0; sn < ns; ++sn)
+    for (int64_t i = start[sn]; i < start[sn] + size[sn]; ++i)
+      for (int64_t q = L.indptr[i]; q < L.indptr[i + 1]; ++q)
+        if (L.indices[q] < start[sn]) ++extb[sn_of[L.indices[q]]];
   const int64_t split_min = getenv("BD_SUPER_SPLIT") ? atoll(getenv("BD_SUPER_SPLIT")) : 8192;
   // dense block of supernode sn: D[k][j] (j <= k) = L[start+k][start+j], the
   // last k+1 entries of the row (diagonal last)
   auto dense = [&](int64_t c0, int64_t k, int64_t j) -> long double {
     return L.values[L.indptr[c0 + k + 1] - 1 - k + j];
   };
-  auto order = [&](const std::vector<int32_t>& lv, DevSuper* out, bool split) -> bd_status {
+  auto order = [&](const std::vector<int32_t>& lv, DevSuper* out, bool split,
+                   const std::vector<int64_t>& ext) -> bd_status {
     std::vector<int32_t> idx(ns);
     std::iota(idx.begin(), idx.end(), 0);
     // lanes per small supernode: one warp each by default; BD_SUPER_PACK=1
@@ -728,8 +736,10 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
     out->grid = (int)std::max<int64_t>(1, std::min<int64_t>(out->ntasks, (int64_t)ctx->nsm * 2));
     return BD_OK;
   };
-  TRY(order(lvf, fw, !getenv("BD_SUPER_NOSPLIT")));
-  TRY(order(lvb, bw, false));
+  TRY(order(lvf, fw, !getenv("BD_SUPER_NOSPLIT"), ext));
+  TRY(order(lvb, bw, !getenv("BD_SUPER_NOSPLIT") &&
+                         !(getenv("BD_SUPER_SPLITB") && atoi(getenv("BD_SUPER_SPLITB")) == 0),
+            extb));
   if (getenv("BD_DEBUG")) {
     int64_t big = 0, maxsz = 0, rows_big = 0;
     for (int64_t s = 0; s < ns; ++s) {
@@ -1473,7 +1483,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     LAUNCHED(ctx);
     dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
                      p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm,
-                     nullptr,           nullptr,        nullptr,      nullptr,
+                     p->SU.task_kind,   p->SU.task_arg, p->SU.sn_cnt, p->rext,
                      p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w};
     dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
         tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
@@ -2218,7 +2228,7 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
     const char* m = getenv("BD_EXACT_TRSV");
     if (!(m && std::string(m) == "rows")) {
       st = build_super(ctx, lower, &p->SL, &p->SU);
-      if (st == BD_OK && p->SL.task_kind && dalloc(&p->rext, lower.n))
+      if (st == BD_OK && (p->SL.task_kind || p->SU.task_kind) && dalloc(&p->rext, lower.n))
         st = fail(ctx, BD_ECUDA, "supernodal solve: allocation failed");
       if (st == BD_OK) p->super = true;
     }
