@@ -179,6 +179,8 @@ struct DevSuper {
   int* sn_size = nullptr;
   int* task_sn = nullptr;
   int* task_w = nullptr;  // lanes per small supernode of each task (nullptr: 32)
+  double* sinv = nullptr;      // whole-block inverses of the largest supernodes
+  long long* sn_inv = nullptr;
   int ntasks = 0;
   int grid = 0;
 };
@@ -722,6 +724,45 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
         CK(ctx, upload_vec(&out->sn_pan, pan));
       }
     }
+    // whole diagonal-block inverses (solve order, packed lower rows) for the
+    // supernodes of at least BD_SUPER_INV_MIN rows: their dense phase becomes
+    // one GEMV instead of ns/32 dependent panel steps
+    {
+      const int64_t inv_min = getenv("BD_SUPER_INV_MIN") ? atoll(getenv("BD_SUPER_INV_MIN")) : 128;
+      std::vector<long long> off(ns, -1);
+      long long tot = 0;
+      std::vector<int64_t> which;
+      for (int64_t k = 0; k < ns; ++k)
+        if (inv_min > 0 && sz[k] >= inv_min && sz[k] > 32) {
+          off[k] = tot;
+          tot += (long long)sz[k] * (sz[k] + 1) / 2;
+          which.push_back(k);
+        }
+      if (tot > 0) {
+        std::vector<double> sinv((size_t)tot);
+        const bool fwd = out == fw;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t w = 0; w < (int64_t)which.size(); ++w) {
+          const int64_t k = which[w], c0 = st[k], m = sz[k];
+          std::vector<long double> B((size_t)m * m), X((size_t)m * m, 0.0L);
+          for (int64_t l = 0; l < m; ++l)
+            for (int64_t q = 0; q <= l; ++q)
+              B[l * m + q] = fwd ? dense(c0, l, q) : dense(c0, m - 1 - q, m - 1 - l);
+          // X = B^{-1} column by column (forward substitution)
+          for (int64_t q = 0; q < m; ++q)
+            for (int64_t l = q; l < m; ++l) {
+              long double acc = (l == q) ? 1.0L : 0.0L;
+              for (int64_t j = q; j < l; ++j) acc -= B[l * m + j] * X[j * m + q];
+              X[l * m + q] = acc / B[l * m + l];
+            }
+          double* dst = sinv.data() + off[k];
+          for (int64_t l = 0; l < m; ++l)
+            for (int64_t q = 0; q <= l; ++q) dst[l * (l + 1) / 2 + q] = (double)X[l * m + q];
+        }
+        CK(ctx, upload_vec(&out->sinv, sinv));
+        CK(ctx, upload_vec(&out->sn_inv, off));
+      }
+    }
     CK(ctx, upload_vec(&out->sn_start, st));
     CK(ctx, upload_vec(&out->sn_size, sz));
     CK(ctx, upload_vec(&out->task_sn, tasks));
@@ -770,6 +811,8 @@ void free_super(DevSuper* s) {
   cudaFree(s->sn_size);
   cudaFree(s->task_sn);
   cudaFree(s->task_w);
+  cudaFree(s->sinv);
+  cudaFree(s->sn_inv);
 }
 
 bd_status upload_cluster(bd_ctx* ctx, const ClusterSchedule& cs, DevCluster* out) {
@@ -1475,7 +1518,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tl{(int)p->n,        p->L.rowptr,  p->L.col,    p->L.val, p->SL.sn_start,
                      p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr,
                      p->SL.task_kind,   p->SL.task_arg, p->SL.sn_cnt, p->rext,
-                     p->SL.pinv,        p->SL.sn_pan,  p->SL.task_w};
+                     p->SL.pinv,        p->SL.sn_pan,  p->SL.task_w, p->SL.sinv, p->SL.sn_inv};
     dev::k_trsv_super<true, Rhs><<<p->SL.grid, 512, 0, st>>>(tl, rhs, p->y_int, nullptr, c, ctr0,
                                                               ctr0 + 1);
     LAUNCHED(ctx);
@@ -1484,7 +1527,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
                      p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm,
                      p->SU.task_kind,   p->SU.task_arg, p->SU.sn_cnt, p->rext,
-                     p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w};
+                     p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w, p->SU.sinv, p->SU.sn_inv};
     dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
         tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
     LAUNCHED(ctx);

@@ -1745,6 +1745,11 @@ struct SuperTri {
   const double* pinv;
   const int* sn_pan;
   const int* task_w;  // small-supernode tasks: lanes per supernode (nullable: 32)
+  // dense phase of the largest supernodes (nullable): the whole diagonal
+  // block's inverse in solve order, packed lower rows (row l at l(l+1)/2),
+  // starting at sn_inv[supernode] (-1: panels)
+  const double* sinv;
+  const long long* sn_inv;
 };
 
 constexpr int SN_MAX = 1024;
@@ -1974,6 +1979,34 @@ __global__ void __launch_bounds__(512, 2) k_trsv_super(SuperTri t, Rhs rhs, doub
     __syncthreads();
     unsigned long long t_ext = 0;
     if (trace && threadIdx.x == 0) t_ext = gtimer();
+    const long long inv_off = t.sn_inv ? t.sn_inv[s0] : -1;
+    if (inv_off >= 0) {
+      // (2') dense block through its precomputed inverse: x_l = sum_{m<=l}
+      //      X[l][m] r_m, two rows per warp in flight, lane-strided rows
+      const double* X = t.sinv + inv_off;
+      for (int l0 = warp; l0 < ns; l0 += 2 * nw) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = l0 + h * nw;
+          if (l < ns) {
+            const double* xr = X + (long long)l * (l + 1) / 2;
+            for (int m = lane; m <= l; m += 32)
+              acc[h] = fma(__ldg(&xr[m]), r[LOWER ? m : ns - 1 - m], acc[h]);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = l0 + h * nw;
+          const double v = group_sum<32>(acc[h]);
+          if (lane == 0 && l < ns) {
+            const int i = c0 + (LOWER ? l : ns - 1 - l);
+            publish(&x[i], v);
+            if (out) out[t.perm ? t.perm[i] : i] = v;
+          }
+        }
+      }
+    } else
     // (2) dense block, left-looking 32-row panels (solve order: ascending rows
     //     for L, descending for U).  r[k] holds row k's rhs, then its solution.
     for (int p0 = 0; p0 < ns; p0 += 32) {

@@ -48,15 +48,19 @@ def test_tile_kernel_matches_oracle(problems, name, kernel, inbox, monkeypatch, 
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("dense_max,pack", [("0", "0"), ("0", "1"), ("100000", "0")])
+@pytest.mark.parametrize("dense_max,pack,inv_min", [("0", "0", "128"), ("0", "1", "128"),
+                                                     ("0", "0", "33"), ("0", "0", "0"),
+                                                     ("100000", "0", "128")])
 @pytest.mark.parametrize("name", ["slab", "torso"])
-def test_exact_inner_paths_match_oracle(problems, name, dense_max, pack, monkeypatch, rng):
+def test_exact_inner_paths_match_oracle(problems, name, dense_max, pack, inv_min, monkeypatch, rng):
     """The exact inner as supernodal passes (BD_EXACT_DENSE_MAX=0: split
     external phases, panel inverses; BD_SUPER_PACK=1: several small supernodes
-    per warp) and as the dense explicit inverse all give the oracle's exact
-    solve (1e-10 relative)."""
+    per warp; BD_SUPER_INV_MIN: whole-block inverses from that size, 0 = none)
+    and as the dense explicit inverse all give the oracle's exact solve (1e-10
+    relative)."""
     monkeypatch.setenv("BD_EXACT_DENSE_MAX", dense_max)
     monkeypatch.setenv("BD_SUPER_PACK", pack)
+    monkeypatch.setenv("BD_SUPER_INV_MIN", inv_min)
     g, _, _ = problems[name]
     ref = orc.make_inner("exact", g)
     ex = bd.ExactFactorization()
