@@ -17,8 +17,10 @@
  *    to the device and owns the copy.
  *  - Every call is asynchronous on the handle's context stream except the ones
  *    documented as synchronising (they return host-visible results).
- *  - Every function returns a bd_status; on failure bd_last_error(ctx) holds a
- *    message.  Handles are thread-compatible, not thread-safe.
+ *  - Every function returns a bd_status; on failure bd_last_error(ctx) holds
+ *    the message of the calling thread's last failing call.  Handles are
+ *    thread-compatible, not thread-safe; different handles may be set up on
+ *    different threads at once.
  */
 #ifndef BIDOMAIN_B200_H
 #define BIDOMAIN_B200_H

@@ -27,5 +27,7 @@ from .simulate import (ActivationMap, SimState, SimulationResult, SimulationSetu
 
 from .vtkio import read_mesh_vtk, write_activation_csv, write_fields_vtk, write_mesh_vtk
 from . import study, vtkio  # bd/bench.py study harness, bd/vtkio.py formats
+from .study import (BenchConfig, BenchRecord, ScalingStudy, calibrate_costs,  # noqa: E402
+                    growth_rate, least_squares_slope, run_scaling_study, save_study)
 
 __version__ = "0.1.0"

@@ -12,7 +12,10 @@ csrc/bd_assembly.cuh): the element tensors are formed once
 on the host, local matrices / gradients / harmonic means and the
 COO -> CSR reduction (stable radix sort, sequential per-entry sums in element
 order) run on the device.  Entries agree with the host path to rounding
-(different summation order); the lumped mass is summed in the reference order.
+(different summation order); entries whose contributions cancel in exact
+arithmetic are stored as exactly 0.0, as the host sum gives them, so the
+zero-dropping CSR adds downstream (grounding, K_m) produce the host's IC(0)
+patterns.  The lumped mass is summed in the reference order.
 """
 from __future__ import annotations
 

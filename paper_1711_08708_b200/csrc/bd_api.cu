@@ -12,9 +12,12 @@
 #include <cstdio>
 #include <cstring>
 #include <future>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
+
+#include <unistd.h>
 
 #include "../../include/bidomain_b200.h"
 #include "bd_assembly.cuh"
@@ -263,8 +266,14 @@ struct bd_prec {
 // ---------------------------------------------------------------------------
 namespace {
 
+// The message of the last failing call, per calling thread: the bulk and
+// Schur inners of one preconditioner are set up on two threads at once
+// (precond.py), and each caller reads its own error right after its call.
+thread_local std::string tl_err;
+
 bd_status fail(bd_ctx* ctx, bd_status st, const std::string& msg) {
-  if (ctx) ctx->err = msg;
+  (void)ctx;
+  tl_err = msg;
   return st;
 }
 
@@ -1093,14 +1102,23 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
   auto kg = dev::k_trsv_btile<dev::RhsGather>;
   auto kv = dev::k_trsv_btile<dev::RhsVec>;
   auto ks = dev::k_trsv_btile<dev::RhsSchur>;
-  // the attribute is per kernel, shared by every schedule: only ever raise it
-  static size_t smem_attr = 0;
-  if (out->smem > smem_attr) {
-    const int sm = (int)out->smem;
-    CK(ctx, cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CK(ctx, cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CK(ctx, cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    smem_attr = out->smem;
+  // the attribute is per kernel and device, shared by every schedule: only
+  // ever raise it (check-and-set under a lock: two inners may be set up on
+  // two threads at once)
+  {
+    static std::mutex mu;
+    static size_t smem_attr[64] = {};
+    int dev_id = 0;
+    CK(ctx, cudaGetDevice(&dev_id));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = smem_attr[dev_id & 63];
+    if (out->smem > cur) {
+      const int sm = (int)out->smem;
+      CK(ctx, cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(ctx, cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(ctx, cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      cur = out->smem;
+    }
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, out->threads, out->smem);
@@ -1888,7 +1906,7 @@ bd_status bd_ctx_synchronize(bd_ctx* c) {
   return BD_OK;
 }
 
-const char* bd_last_error(bd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+const char* bd_last_error(bd_ctx* c) { return c ? tl_err.c_str() : "null context"; }
 
 int64_t bd_launch_count(bd_ctx* c) { return c ? c->launches : 0; }
 
@@ -2232,12 +2250,22 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
   const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 16384;
+  // the explicit inverse takes n^2 doubles on the host and on the device:
+  // only when both have 4x that free (else the supernodal solves below)
+  bool dense_fits = false;
   if (st == BD_OK && kind == BD_INNER_EXACT && n <= dense_max) {
+    const double bytes = 8.0 * (double)n * (double)n;
+    size_t dfree = 0, dtotal = 0;
+    const double hfree = (double)sysconf(_SC_AVPHYS_PAGES) * (double)sysconf(_SC_PAGESIZE);
+    dense_fits = cudaMemGetInfo(&dfree, &dtotal) == cudaSuccess && 4.0 * bytes <= (double)dfree &&
+                 4.0 * bytes <= hfree;
+  }
+  if (st == BD_OK && kind == BD_INNER_EXACT && dense_fits) {
     // explicit inverse of P A P^T from the sparse factor, one column per host
     // thread (X^T = X up to rounding; row j of X holds the solve with e_j)
     std::vector<double> X((size_t)n * n);
     int bad = 0;
-#pragma omp parallel
+#pragma omp parallel reduction(| : bad)
     {
       std::vector<double> w(n);
 #pragma omp for schedule(dynamic, 8)
@@ -2701,13 +2729,13 @@ bd_status bd_pcg_solve(bd_system* s, bd_prec* p, const double* b, const double* 
       std::snprintf(buf, sizeof buf, "non-finite residual");
     else
       std::snprintf(buf, sizeof buf, "conjugate gradient breakdown: curvature %g", hsc[dev::S_CURV]);
-    ctx->err = buf;
+    tl_err = buf;
   } else if (!hflag[dev::F_CONV]) {
     st = BD_ENOCONV;
     char buf[160];
     std::snprintf(buf, sizeof buf, "PCG did not reach tol=%g within %lld iterations (residual %.3e)",
                   tol, (long long)max_iter, stats->final_residual);
-    ctx->err = buf;
+    tl_err = buf;
   }
   stats->status = st;
   stats->wall_ms =

@@ -272,25 +272,48 @@ class BlockLUPreconditioner:
         self.ctx = nat.ctx
 
     # -- counters (bd/precond.py:272-279) ----------------------------------------
+    # The device counts applications inside the captured PCG loop; the
+    # reference's counters are plain assignable attributes, so an assignment
+    # is kept as a host-side offset on top of the device count.
     def _counters(self):
         buf = (C.c_int64 * 3)()
         _lib.check(_lib.lib().bd_blocklu_counters(self.handle, buf), self.ctx.handle)
-        return list(buf)
+        off = self.__dict__.get("_count_off", (0, 0, 0))
+        return [int(b) + o for b, o in zip(buf, off)]
+
+    def _set_counter(self, i: int, value: int) -> None:
+        cur = self._counters()
+        off = list(self.__dict__.get("_count_off", (0, 0, 0)))
+        off[i] += int(value) - cur[i]
+        self._count_off = tuple(off)
 
     @property
     def p1_count(self) -> int:
         return self._counters()[0]
 
+    @p1_count.setter
+    def p1_count(self, value: int) -> None:
+        self._set_counter(0, value)
+
     @property
     def pk_count(self) -> int:
         return self._counters()[1]
+
+    @pk_count.setter
+    def pk_count(self, value: int) -> None:
+        self._set_counter(1, value)
 
     @property
     def si_count(self) -> int:
         return self._counters()[2]
 
+    @si_count.setter
+    def si_count(self, value: int) -> None:
+        self._set_counter(2, value)
+
     def reset_counters(self) -> None:
         _lib.check(_lib.lib().bd_blocklu_reset_counters(self.handle), self.ctx.handle)
+        self._count_off = (0, 0, 0)
 
     # -- applications ----------------------------------------------------------------
     def _bulk_inverse(self, y):

@@ -2,8 +2,10 @@
 the host assembly that is bit-identical to the reference
 (tests/test_host.py::test_builders_and_assembly_bit_identical_to_reference).
 
-Same sparsity pattern (explicit zeros kept, as the reference's COO -> CSR);
-entries within 1e-13 of the row scale (different summation order); lumped
+Same sparsity pattern (explicit zeros kept, as the reference's COO -> CSR)
+and the SAME exact zeros (entries whose contributions cancel are stored as
+0.0, so the zero-dropping CSR adds of grounding and K_m give the host's IC(0)
+patterns); entries within 1e-13 of the row scale (different summation order); lumped
 masses within 1e-13 relative; deterministic run to run; a time step on the
 device-assembled system within the BASELINE parity tolerances of the host one."""
 import numpy as np
@@ -26,6 +28,8 @@ CASES = {
     "cfg1_64": lambda: (lambda w: (w.mesh, w.params, w.fibers))(configs.cfg1(64)),
     "cfg2_8": lambda: (lambda w: (w.mesh, w.params, w.fibers))(configs.cfg2((8, 8, 4))),
     "cfg4_12": lambda: (lambda w: (w.mesh, w.params, w.fibers))(configs.cfg4(12)),
+    "cfg2_32": lambda: (lambda w: (w.mesh, w.params, w.fibers))(configs.cfg2((32, 32, 16))),
+    "cfg4_24": lambda: (lambda w: (w.mesh, w.params, w.fibers))(configs.cfg4(24)),
 }
 
 
@@ -36,8 +40,8 @@ def _same(dev, host):
     scale = np.repeat(np.maximum(abs(host).max(axis=1).toarray().ravel(), 1e-300),
                       np.diff(host.indptr))
     assert (np.abs(dev.data - host.data) <= 1e-13 * scale).all()
-    # (which entries round to exactly 0.0 depends on the summation order, so
-    # the two may differ there; tests/test_gpu_fullsize_cfg4.py bounds the effect)
+    # the exact zeros (cancellations) coincide, so zero-dropping adds agree
+    np.testing.assert_array_equal(dev.data == 0.0, host.data == 0.0)
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
@@ -55,6 +59,11 @@ def test_device_blocks_match_host(case):
     km_h = build_monodomain_matrix(mesh, params, 4000.0, fibers)
     km_d = build_monodomain_matrix(mesh, params, 4000.0, fibers, assembly="device")
     _same(km_d, km_h)
+    # the grounded S_1 (the bulk IC(0) input) has the host's pattern
+    from paper_1711_08708_b200.precond import regularize_stiffness
+    g_h = regularize_stiffness(assemble_stiffness(mesh, TensorField(params, d, "bar1", fibers)))
+    g_d = regularize_stiffness(da.stiffness("bar1"))
+    _same(g_d.grounded(), g_h.grounded())
 
 
 def test_device_assembly_deterministic():

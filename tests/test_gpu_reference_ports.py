@@ -83,6 +83,20 @@ def test_warm_start_and_counters(sys2d, rng):
     assert st2.iterations == 0
 
 
+def test_counters_are_assignable(sys2d, rng):
+    """p1_count / pk_count / si_count are plain attributes in the reference
+    (bd/precond.py:272-279): assignment sticks and later applications add on."""
+    pre = bd.BlockLUPreconditioner(sys2d, inner="jacobi")
+    pre.p1_count, pre.pk_count, pre.si_count = 10, 20, 30
+    assert (pre.p1_count, pre.pk_count, pre.si_count) == (10, 20, 30)
+    pre.apply_inverse(range_rhs(sys2d, rng))
+    assert (pre.p1_count, pre.pk_count, pre.si_count) == (12, 21, 32)
+    _, st = bd.pcg_solve(sys2d, pre, range_rhs(sys2d, rng), tol=1e-8, max_iter=5000)
+    assert st.p1_count == 2 * st.iterations and pre.p1_count == 12 + 2 * st.iterations
+    pre.reset_counters()
+    assert (pre.p1_count, pre.pk_count, pre.si_count) == (0, 0, 0)
+
+
 def test_dump_residuals(sys2d, pre_exact, rng, tmp_path):
     _, st = bd.pcg_solve(sys2d, pre_exact, range_rhs(sys2d, rng))
     path = tmp_path / "residuals.csv"

@@ -69,3 +69,21 @@ def test_exact_inner_paths_match_oracle(problems, name, dense_max, pack, inv_min
         y = rng.standard_normal(g.shape[0])
         got, want = ex.apply_inverse(y), ref.apply(y)
         assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("mode", ["dtile", "persist", "syncfree", "tiled", "rows", "cluster"])
+@pytest.mark.parametrize("name", ["slab", "torso"])
+def test_fallback_schedules_match_oracle(problems, name, mode, monkeypatch, rng):
+    """The non-default triangular-solve schedules (BD_TRSV):
+    dtile and persist are the live fallbacks when a blocked-tile schedule
+    cannot be built, syncfree (any other value) is the level-free v0 kernel
+    pair; tiled / rows / cluster are the cooperative and cluster variants.
+    Each must give the oracle's IC(0) application (1e-12 relative)."""
+    monkeypatch.setenv("BD_TRSV", mode)
+    g, xyz, ref = problems[name]
+    ic = bd.IncompleteCholesky0()
+    ic.setup(g, coords=xyz)
+    for _ in range(3):
+        y = rng.standard_normal(g.shape[0])
+        got, want = ic.apply_inverse(y), ref.apply(y)
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()

@@ -66,6 +66,14 @@ def test_unknown_inner_name():
         bd.make_inner("amg")
 
 
+def test_study_names_at_package_root():
+    """The reference re-exports its study harness at the root (bd/__init__.py:29-30)."""
+    import paper_1711_08708_b200 as bd
+    for name in ("BenchConfig", "BenchRecord", "ScalingStudy", "calibrate_costs", "growth_rate",
+                 "run_scaling_study"):
+        assert getattr(bd, name) is getattr(bd.study, name)
+
+
 def test_gamma():
     assert bd.gamma(500.0, 1.0, 0.2) == pytest.approx(2500.0)
     assert bd.gamma(200.0, 1.0, 0.05) == pytest.approx(4000.0)
