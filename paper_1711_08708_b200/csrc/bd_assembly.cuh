@@ -166,18 +166,9 @@ __global__ void __launch_bounds__(256) k_seg_start(int64_t np, const long long* 
     if (head[p]) start[pos[p]] = p;
 }
 
-// Entries whose element contributions cancel in exact arithmetic (edges of the
-// structured meshes where the orthotropic / rotated tensors give equal and
-// opposite couplings) come out of the host assembly as exactly 0.0, and the
-// reference's CSR adds (bd/precond.py:44-46, 72-75: grounding, K_m) then DROP
-// them from the IC(0) pattern.  Summed in a different order here they would be
-// rounding residues (~1e-16 of Σ|c|) and stay in the pattern, changing the
-// incomplete factor at O(1).  So an entry with |Σc| <= kSnapRel·Σ|c| is stored
-// as exactly 0.0.  tools/hostcheck/zero_pattern.py measures the margin on the
-// BASELINE meshes: every host zero is such a cancellation, no kept host entry
-// is below 1e-12·Σ|c| (the smallest is ~1e-3), and device residues are
-// ~1e-15·Σ|c|.
-constexpr double kSnapRel = 1e-10;
+// (Entries whose contributions cancel in exact arithmetic come out as rounding
+// residues here; the host side, assembly.py DeviceAssembler._reference_zeros,
+// gives them the reference's own value, exact zero or residue.)
 
 // one thread per CSR entry: sequential sum of its contributions (element
 // order); diagonal entries also form the lumped mass in (local vertex, element)
@@ -198,14 +189,9 @@ __global__ void __launch_bounds__(256) k_segsum(int64_t nnz, int64_t np, int64_t
     const int64_t s0 = start[u], s1 = u + 1 < nnz ? start[u + 1] : np;
     const unsigned long long key = keys[s0];
     const int64_t r = (int64_t)(key / (unsigned long long)nv), c = (int64_t)(key % (unsigned long long)nv);
-    double s = 0.0, a = 0.0;
-    for (int64_t q = s0; q < s1; ++q) {
-      const double c = local[vals[q]];
-      s += c;
-      a += fabs(c);
-    }
-    // exact-arithmetic cancellation -> exactly 0.0 (see kSnapRel)
-    data[u] = fabs(s) <= kSnapRel * a ? 0.0 : s;
+    double s = 0.0;
+    for (int64_t q = s0; q < s1; ++q) s += local[vals[q]];
+    data[u] = s;
     col[u] = (int)c;
     ukey[u] = key;
     if (r == c) {

@@ -3,9 +3,10 @@ the host assembly that is bit-identical to the reference
 (tests/test_host.py::test_builders_and_assembly_bit_identical_to_reference).
 
 Same sparsity pattern (explicit zeros kept, as the reference's COO -> CSR)
-and the SAME exact zeros (entries whose contributions cancel are stored as
-0.0, so the zero-dropping CSR adds of grounding and K_m give the host's IC(0)
-patterns); entries within 1e-13 of the row scale (different summation order); lumped
+and the SAME values, bit for bit, at the entries whose contributions cancel
+in exact arithmetic (exact zeros and the reference's ~1e-32 rounding
+residues), so the zero-dropping CSR adds of grounding and K_m give the
+host's IC(0) patterns; entries within 1e-13 of the row scale (different summation order); lumped
 masses within 1e-13 relative; deterministic run to run; a time step on the
 device-assembled system within the BASELINE parity tolerances of the host one."""
 import numpy as np
@@ -40,8 +41,11 @@ def _same(dev, host):
     scale = np.repeat(np.maximum(abs(host).max(axis=1).toarray().ravel(), 1e-300),
                       np.diff(host.indptr))
     assert (np.abs(dev.data - host.data) <= 1e-13 * scale).all()
-    # the exact zeros (cancellations) coincide, so zero-dropping adds agree
+    # exact-arithmetic cancellations: the same exact zeros and the same
+    # rounding residues, bit for bit, so the zero-dropping adds agree
     np.testing.assert_array_equal(dev.data == 0.0, host.data == 0.0)
+    tiny = np.abs(host.data) <= 1e-10 * scale
+    np.testing.assert_array_equal(dev.data[tiny], host.data[tiny])
 
 
 @pytest.mark.parametrize("case", sorted(CASES))

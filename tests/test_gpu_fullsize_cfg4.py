@@ -9,9 +9,11 @@ run recorded by `tools/oracle_fullsize.py --config cfg4 --cells 96`
   subsample) within 1e-8 — the BASELINE parity targets (measured: 2e-16..2e-13);
 * the P1 blocks assembled on the device (the path bench.py times): the same
   bounds, state within 1e-8.  The device sums element contributions in a
-  different order and stores exact-arithmetic cancellations as exactly 0.0
-  (csrc/bd_assembly.cuh, kSnapRel), so the zero-dropping CSR adds give the
-  reference's IC(0) patterns and the two solves agree to rounding."""
+  different order; the entries that cancel in exact arithmetic (in the
+  isotropic torso of this mesh the reference's own sum leaves most of them as
+  ~1e-17 residues, which its zero-dropping CSR adds keep in the IC(0)
+  pattern) take the reference-order value on the host
+  (assembly.reference_order_values), so the two solves agree to rounding."""
 import json
 import os
 

@@ -225,3 +225,30 @@ def test_activation_times_kats(rng):
     for k in range(1, 20):
         tr.record(history[k - 1], history[k], (k - 1) * 0.25, 0.25)
     np.testing.assert_array_equal(tr.result().phi, batch.phi)
+
+
+def test_reference_order_values_bit_identical():
+    """The device assembly's cancelled entries are re-evaluated on the host in
+    the reference's summation order (assembly.reference_order_values): on a
+    heart-in-torso box, where the reference's own sum leaves some exact
+    cancellations as ~1e-32 residues and others as exact zeros, the re-evaluated
+    values equal the full host assembly bit for bit."""
+    import scipy.sparse as sp
+    from paper_1711_08708_b200 import configs
+    from paper_1711_08708_b200.assembly import (Space, _grads_volumes, assemble_stiffness,
+                                                reference_order_values)
+    from paper_1711_08708_b200.conductivity import TensorField
+    wl = configs.cfg4(24)
+    f = TensorField(wl.params, 3, "bar1", wl.fibers)
+    s = assemble_stiffness(wl.mesh, f, Space.FULL).tocoo()
+    el = wl.mesh.elements
+    g, v = _grads_volumes(wl.mesh.vertices, el, 3)
+    sig = f.evaluate_batch(wl.mesh.vertices[el].mean(axis=1), wl.mesh.tags)
+    loc = np.abs(np.einsum("eid,edk,ejk->eij", g, sig, g) * v[:, None, None])
+    b = sp.coo_matrix((loc.ravel(), (np.repeat(el, 4, axis=1).ravel(), np.tile(el, (1, 4)).ravel())),
+                      shape=s.shape).tocsr()
+    bs = np.asarray(b[s.row, s.col]).ravel()
+    cand = np.abs(s.data) <= 1e-10 * bs
+    assert cand.sum() > 100 and (s.data[cand] != 0).sum() > 0  # zeros AND residues present
+    got = reference_order_values(wl.mesh, f, Space.FULL, s.row[cand], s.col[cand])
+    np.testing.assert_array_equal(got.view(np.int64), s.data[cand].view(np.int64))

@@ -58,6 +58,9 @@ def check(name, mesh, field, space):
     print(f"{name}: nnz(b)={b.nnz} nnz(host)={s.nnz} explicit_zero_in_host={(s.data == 0).sum()} "
           f"cancelled={zero.sum()} residues_kept(<1e-12)={small.sum()} "
           f"min kept |s|/b={kept.min():.3e} max cancelled... ({time.time() - t0:.0f}s)", flush=True)
+    pos = r[r > 0]
+    h, e = np.histogram(np.log10(pos), bins=np.arange(-17, 1))
+    print("   log10(|s|/b) histogram:", {int(a): int(c) for a, c in zip(e[:-1], h) if c})
     return r, zero
 
 
