@@ -365,6 +365,9 @@ def pcg(S1, Si, mh, mass, gam, prec: BlockLU, bu, bv, tol=1e-6, max_iter=500, x0
         dv = zv + beta * dv
     fin()
     if not st["converged"]:
+        # the normalised iterate after max_iter iterations (iteration-level
+        # parity at sizes where a full solve is out of reach on the CPU)
+        st["iterate"] = normalize(mass, xu, xv)
         raise OracleNoConvergence(f"PCG did not reach tol={tol} within {max_iter} iterations", st)
     return normalize(mass, xu, xv), st
 

@@ -193,6 +193,7 @@ struct bd_inner {
   int kind;
   int64_t n;
   int G = 8;
+  int prof_cls = 2;  // profile class of its triangular passes (2 bulk, 3 Schur)
   DevTri L, U;
   bool super = false;
   DevSuper SL, SU;
@@ -1482,16 +1483,22 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
                                                                   dev::SENTINEL, c);
     LAUNCHED(ctx);
+    prof_mark(ctx, 5);  // (profile classes: fills and dots are vector work,
+                        //  the two passes alone are the triangular-solve class)
     if (!Rhs::kScalar && p->rhs_pre)
       TRY(launch_btile(p, p->BL, dev::RhsVec{p->rhs_pre, (int)p->n, nullptr, nullptr}, p->y_int, c,
                        ctr0, ctr0 + 1, nullptr));
     else
       TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr));
+    prof_mark(ctx, p->prof_cls);
     dev::k_fill<<<grid_for(ctx, nf2, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : xg, nf2,
                                                                   dev::SENTINEL, c);
     LAUNCHED(ctx);
+    prof_mark(ctx, 5);
     TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr));
+    prof_mark(ctx, p->prof_cls);
     if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
+    prof_mark(ctx, 5);
     return BD_OK;
   }
   if (p->dtile) {
@@ -2469,6 +2476,8 @@ bd_status bd_blocklu_create(bd_system* s, bd_inner* bulk, bd_inner* schur, doubl
   p->sys = s;
   p->bulk = bulk;
   p->schur = schur;
+  bulk->prof_cls = 2;
+  schur->prof_cls = 3;
   p->beta = beta;
   const int64_t n = s->n, m = s->m, nm = n + m;
   int64_t parts = (int64_t)ctx->nsm * 8 * 2;
@@ -2669,14 +2678,17 @@ bd_status bd_pcg_solve(bd_system* s, bd_prec* p, const double* b, const double* 
     ctx->launches += 1;
     it_launch = -1;  // counted from the iteration count below
   } else {
-    int batch = 2;
+    // (profile mode: one iteration per host round trip, so every profiled
+    // iteration is a real one; the host gap before it goes to class 7)
+    int batch = ctx->profile ? 1 : 2;
     for (;;) {
+      prof_mark(ctx, 7);
       for (int i = 0; i < batch; ++i) TRY(enqueue_iteration(p));
       CK(ctx, cudaMemcpyAsync(hflag, c.fl, sizeof(int) * dev::NFLAGS, cudaMemcpyDeviceToHost,
                               ctx->stream));
       CK(ctx, cudaStreamSynchronize(ctx->stream));
       if (hflag[dev::F_DONE] || hflag[dev::F_STOP]) break;
-      batch = std::min(batch * 2, 32);
+      if (!ctx->profile) batch = std::min(batch * 2, 32);
     }
   }
   // x <- normalize(x) (bd/system.py:138-146), zero for a zero rhs
