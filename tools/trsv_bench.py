@@ -22,8 +22,15 @@ rng = np.random.default_rng(0)
 y = torch.as_tensor(rng.standard_normal(g.shape[0])).cuda()
 res = {}
 for mode in os.environ.get("MODES", "persist,tiled,syncfree").split(","):
-    base, _, kern = mode.partition("@")  # e.g. btile@smem / btile@reg
+    mode_k, _, ring = mode.partition("%")  # e.g. btile@reg%static+persm3
+    base, _, kern = mode_k.partition("@")  # e.g. btile@smem / btile@reg
     os.environ["BD_TRSV"] = base
+    # suffix knobs: %static / %dyn (BD_RT_STATIC), %persmN (BD_BTILE_PERSM)
+    for knob in filter(None, ring.split("+")):
+        if knob in ("static", "dyn"):
+            os.environ["BD_RT_STATIC"] = "1" if knob == "static" else "0"
+        elif knob.startswith("persm"):
+            os.environ["BD_BTILE_PERSM"] = knob[5:]
     if kern:
         os.environ["BD_BTILE_KERNEL"] = kern
     inner = bd.IncompleteCholesky0(); t0 = time.time(); inner.setup(g, coords=wl.mesh.vertices)
