@@ -11,8 +11,11 @@ time loop's unit (bd/simulate.py:134-170).  Inputs are larger than L2
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
                   [--workload cfg0|cfg1|cfg2|cfg3] [--inner ic0|exact|jacobi]
 
-N>1 (torchrun): one process per GPU; round 1 runs independent replicas of
-the workload per GPU (weak scaling, no data-path collective).
+N>1 (torchrun): one process per GPU; the same mesh is partitioned across the
+GPUs (RCB) and solved by the sharded PCG (strong scaling: NCCL halos and four
+all-reduces per iteration, block-Jacobi inners; `--mode replicas` runs N
+independent solves instead).  `--mode sharded` at N=1 runs the sharded engine
+on one rank.
 `--impl reference` times the CPU oracle port (the reference algorithm in
 numpy/scipy, oracle/) on this host, each step a bounded sample of PCG
 iterations extrapolated with the oracle's own iterations per step.
@@ -364,50 +367,38 @@ def run_native(args, rank, world, local_rank):
         emit(line)
 
 
-def weak_cells(base, world):
-    """Refine the base slab so every GPU keeps a base-sized part: double the
-    axis with the most cells per rank first (8 GPUs on (128,128,64) -> the
-    BASELINE config-3 grid (256,256,128))."""
-    cells = list(base)
-    k = 1
-    while k * 2 <= world:
-        ax = min(range(3), key=lambda a: (cells[a] // base[a], a))
-        cells[ax] *= 2
-        k *= 2
-    if world != k:
-        cells[0] = cells[0] * world // k
-    return tuple(cells)
-
-
 def run_sharded(args, rank, world, local_rank):
-    """Mesh partitioned across the GPUs (RCB), NCCL halo exchange + allreduce,
-    block-Jacobi inner solves (paper_1711_08708_b200.distributed).  Weak
-    scaling: the slab is refined with N so each GPU keeps a cfg2-sized part."""
+    """The workload's mesh partitioned across the N GPUs (RCB), STRONG scaling:
+    the same mesh and PCG tolerance at every N.  Each rank runs the native
+    sharded iteration (distributed.NativeShard: bd_shard_* kernels, block-Jacobi
+    inners on its owned blocks; ShardSolver: NCCL halos + four all-reduces per
+    iteration, one iteration captured in a CUDA graph)."""
     import torch
     import torch.distributed as dist
-    from paper_1711_08708_b200 import _lib, configs
+    from paper_1711_08708_b200 import _lib
     from paper_1711_08708_b200 import distributed as D
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     ctx = _lib.Context(local_rank)
     _lib.Context._default = ctx
-    cells = weak_cells((128, 128, 64), world)
-    wl = configs.cfg2(cells, inner=args.inner or "ic0", name="cfg3" if cells == (256, 256, 128) else "cfg2")
+    wl = build_workload(args.workload, args.inner)
     t0 = time.perf_counter()
     part = D.rcb_partition(wl.mesh.vertices, world)
     sim = D.DistributedSimulation(wl, part, rank, world, dist, dev)
     t_setup = time.perf_counter() - t0
-    log(f"[rank {rank}] sharded {cells}: n_own={sim.lp.n_own} ghosts={sim.lp.ghosts.size} "
-        f"setup {t_setup:.1f}s")
+    lp = sim.lp
+    log(f"[rank {rank}] sharded {wl.name}: n_own={lp.n_own} m_own={lp.m_own} "
+        f"ghosts={lp.ghosts.size} setup {t_setup:.1f}s")
     state = sim.resting()
     for _ in range(args.warmup):
         state, _ = sim.step(state)
+    saved = tuple(s.clone() if hasattr(s, "clone") else s for s in state)
     torch.cuda.synchronize()
     dist.barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    launches0 = ctx.launches()
+    launches0 = ctx.launches() + sim.solver.replayed_launches
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = []
@@ -415,53 +406,96 @@ def run_sharded(args, rank, world, local_rank):
     for _ in range(args.steps):
         state, st = sim.step(state)
         iters.append(st["iterations"])
-    graph_used, graph_err = st.get("graph"), st.get("graph_error")
     e1.record(stream)
     torch.cuda.synchronize()
+    launches = ctx.launches() + sim.solver.replayed_launches - launches0
     clk = clocks.stop()
     dist.barrier()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    n, m = wl.n, wl.n_heart
-    base_dof = 2 * (129 * 129 * 65)
+
+    def max_over_ranks(v, op=dist.ReduceOp.MAX):
+        t = torch.tensor([float(v)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    ms = max_over_ranks(e0.elapsed_time(e1))
     steps_s = args.steps / (ms / 1e3)
-    # per-GPU HBM GB/s (BASELINE config 3): this rank's algorithmic bytes per
-    # PCG iteration (SURVEY §8d on the local blocks and block-Jacobi factors)
-    # over the measured time per iteration, reported as the minimum over ranks
-    lp = sim.lp
-    try:
-        nnz_l1 = int(sim.prec.bulk.factor_info()["nnz"])
-        nnz_lk = int(sim.prec.schur.factor_info()["nnz"])
-    except Exception:  # non-factor inners (jacobi)
-        nnz_l1 = nnz_lk = 0
-    b_loc = iteration_bytes(lp.n_own, lp.m_own, lp.S1.nnz, lp.Si.nnz, nnz_l1, nnz_lk)
     it_total = max(1.0, float(np.sum(iters)))
-    gbs = torch.tensor([b_loc / (ms / it_total * 1e-3) / 1e9], device=dev, dtype=torch.float64)
-    dist.all_reduce(gbs, op=dist.ReduceOp.MIN)
-    gbs_min = float(gbs.item())
-    value = steps_s * (n + m) / base_dof  # cfg2-equivalent time steps per second (aggregate)
+    ms_iter = ms / it_total
+    # ---- e2e: the same steps through DistributedSimulation.step with host buffers
+    hu = saved[0].cpu().pin_memory()
+    hv = saved[1].cpu().pin_memory()
+    hw = saved[2].cpu().pin_memory()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host = saved[3]
+    e2.record(stream)
+    for _ in range(args.steps):
+        s = (hu.to(dev, non_blocking=True), hv.to(dev, non_blocking=True),
+             hw.to(dev, non_blocking=True), t_host)
+        s, _ = sim.step(s)
+        hu.copy_(s[0], non_blocking=True)
+        hv.copy_(s[1], non_blocking=True)
+        hw.copy_(s[2], non_blocking=True)
+        t_host = s[3]
+    e3.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3))
+    # ---- per-GPU HBM GB/s (BASELINE config 3): the rank's algorithmic bytes per
+    # PCG iteration (SURVEY §8d on its local blocks and block-Jacobi factors)
+    nnz_l1, nnz_lk = sim.shard.factor_nnz()
+    b_loc = iteration_bytes(lp.n_own, lp.m_own, lp.S1.nnz, lp.Si.nnz, nnz_l1, nnz_lk)
+    gbs_min = max_over_ranks(-(b_loc / (ms_iter * 1e-3) / 1e9)) * -1.0
+    peak, peak_kind = measured_peak_hbm()
+    iters_1gpu = None
+    fx = os.path.join(REPO, "tests", "golden", f"{wl.name}_{wl.inner}_oracle.json")
+    if os.path.exists(fx):
+        with open(fx) as fh:
+            ref_it = json.load(fh)["iters"]
+        k0 = args.warmup
+        sel = ref_it[k0: k0 + args.steps] or ref_it
+        iters_1gpu = round(float(np.mean(sel)), 2)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        sysm, km, _ = assemble(wl)
+        cpu = cpu_baseline(sysm, km, wl, iters_1gpu or float(np.mean(iters)), args.cpu_iters)
+    n, m = wl.n, wl.n_heart
+    bytes_in = 8 * (n + 2 * m)
     if rank == 0:
-        emit(({
-            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        emit({
+            "metric": METRIC, "value": round(steps_s, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (deterministic structured mesh)",
-            "config": {"workload": f"{wl.name} slab {cells[0]}x{cells[1]}x{cells[2]} sharded "
-                                   f"(RCB, NCCL halo + allreduce, block-Jacobi {wl.inner})",
-                       "dof": n + m, "raw_steps_per_s": round(steps_s, 4),
-                       "value_definition": "steps/s x dof / dof(cfg2): cfg2-equivalent steps/s",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic structured mesh, seeded/defined stimulus; "
+                    "no dataset)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "dof": n + m, "n": n,
+                       "n_heart": m, "inner": f"block-Jacobi {wl.inner} (one block per GPU)",
+                       "tol": wl.tol, "dt_ms": wl.dt,
+                       "steps_timed": f"{args.warmup + 1}..{args.warmup + args.steps}",
+                       "parallelism": f"mesh partition x{world} (RCB), NCCL halos + 4 "
+                                      "all-reduces per PCG iteration",
                        "pcg_iters_per_step": round(float(np.mean(iters)), 2),
-                       "ms_per_pcg_iter": round(ms / it_total, 4),
-                       "hbm_gbs_per_gpu": round(gbs_min, 1),
-                       "hbm_gbs_definition": "algorithmic bytes per PCG iteration of the rank's "
-                                             "blocks (SURVEY 8d) / time per iteration, min over "
-                                             "ranks",
-                       "pcg_loop": "cuda graph" if graph_used else f"eager ({graph_err})",
-                       "parallelism": f"mesh partition x{world}"},
-            "gpu_launches": int(ctx.launches() - launches0), "clocks": clk,
-            "setup_s": round(t_setup, 1)}))
+                       "pcg_iters_per_step_1gpu": iters_1gpu,
+                       "ms_per_pcg_iter": round(ms_iter, 4),
+                       "l2": "inputs > L2 at N <= 8 (the rank's blocks stream per iteration)"},
+            "e2e": {"value": round(args.steps / (e2e_ms / 1e3), 4), "unit": UNIT,
+                    "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_in,
+                    "note": "DistributedSimulation.step with pinned host (u, v, w) in and out "
+                            "every step (totals over ranks)"},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded PCG iteration per GPU",
+                         "achieved": round(gbs_min, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs_min / peak, 4), "peak_source": peak_kind,
+                         "traffic": None,
+                         "algorithmic_bytes_per_launch": b_loc,
+                         "definition": "algorithmic bytes of one PCG iteration on the rank's "
+                                       "blocks (SURVEY 8d) / time per iteration, min over "
+                                       "ranks"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "setup_s": {"rank0": round(t_setup, 1)},
+            "graph": bool(st.get("graph")), "graph_error": st.get("graph_error"),
+        })
 
 
 def cpu_baseline(sysm, km, wl, iters_per_step, n_iter):
@@ -603,10 +637,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default=os.environ.get("BD_BENCH_MODE"),
                     choices=["replicas", "sharded"],
-                    help="N>1 default 'sharded': the slab partitioned across the GPUs (RCB, "
-                         "NCCL halo + all-reduce; weak scaling, 8 GPUs = config 3); 'replicas': "
-                         "N independent cfg2 solves.  N=1 runs the single-graph cfg2 solve "
-                         "unless --mode sharded is given.")
+                    help="N>1 default 'sharded': the workload's mesh partitioned across the "
+                         "GPUs (RCB, NCCL halos + all-reduces; strong scaling, the same mesh at "
+                         "every N); 'replicas': N independent solves.  N=1 runs the single-GPU "
+                         "engine unless --mode sharded is given.")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -52,6 +52,7 @@ typedef struct bd_csr bd_csr;         /* device CSR matrix */
 typedef struct bd_system bd_system;   /* Λ = [[S_1, Π^T S_i],[S_i Π, γ M_H + S_i]] */
 typedef struct bd_inner bd_inner;     /* exact / ic0 / jacobi inner solve */
 typedef struct bd_prec bd_prec;       /* block-LU preconditioner P_Λ */
+typedef struct bd_shard bd_shard;     /* one rank of the mesh-partitioned PCG */
 
 /* Solve statistics (bd/krylov.py:23-38).  Filled even on error. */
 typedef struct {
@@ -86,8 +87,8 @@ bd_status bd_spmv(bd_csr* a, const double* x, double* y, double alpha, double be
 /* y = alpha * A [x ; x_ghost] + beta * y with the input split in two device
  * arrays: column c < nsplit reads x[c], column c >= nsplit reads
  * x_ghost[c - nsplit] (a sharded rank's owned entries and its halo, without
- * concatenating them).  Needs the ELL copy bd_csr_create builds for short,
- * near-uniform rows (P1 stencils); BD_EINVAL otherwise. */
+ * concatenating them).  Uses the ELL copy bd_csr_create builds for short,
+ * near-uniform rows (P1 stencils), else the CSR rows. */
 bd_status bd_spmv_split(bd_csr* a, const double* x, int64_t nsplit, const double* x_ghost,
                         double* y, double alpha, double beta);
 
@@ -240,6 +241,57 @@ bd_status bd_assemble_destroy(bd_asm* a);
 bd_status bd_step_track(bd_system* s, const double* v_prev, const double* v_new, double* phi,
                         double t_prev, double dt, double threshold, double band_lo,
                         double band_hi, const double* u, double* out);
+
+/* ---- mesh-partitioned PCG, one rank (distributed.py) -------
+ * The deflated PCG (bd/krylov.py:46-140) with the block-LU preconditioner
+ * (bd/precond.py:281-312) on a rank's owned rows [u_own (n) | v_own (m)],
+ * block-Jacobi inners (the owned diagonal blocks), all vector work and
+ * scalars on the device.  The caller interleaves the calls with the halo
+ * exchanges and four all-reduces of the device buffer red (see vectors):
+ *   begin; [halo x0] lambda(x, use_flags=0) (if x0); init; ALLREDUCE red[1..3];
+ *   check(initial=1); pinv1; [halo z1_H] pinv2; [halo s] pinv3;
+ *   ALLREDUCE red[3]; pinv4; ALLREDUCE red[4..6]; finish(initial=1);
+ *   per iteration: [halo d] lambda(d, 1); ALLREDUCE red[0]; update;
+ *   ALLREDUCE red[1..2]; check(0); pinv1; [halo] pinv2; [halo] pinv3;
+ *   ALLREDUCE red[3]; pinv4; ALLREDUCE red[4..6]; finish(0);
+ *   then wmean; ALLREDUCE red[8]; normalize; read.
+ * After convergence / breakdown / max_iter every call is a device no-op, so
+ * a captured iteration may be replayed past the end (done() tells).
+ * S1: n x (n + ghosts), Si: m x (m + heart ghosts); mass / heart_mass
+ * host; msum = global sum of mass;
+ * red: caller-owned device buffer of >= 16 doubles (the reduction slots the
+ * caller all-reduces in place).  Optional (both or neither): Si_ext = S_i
+ * with ghost column j renumbered n + j, and z1ext = a caller-owned device
+ * buffer of n + heart-ghost doubles that holds z1 followed by its halo (the
+ * caller receives the halo there); then pinv2 forms r_v − S_i t inside the
+ * Schur forward pass and ignores its tg argument. */
+bd_status bd_shard_create(bd_ctx* ctx, int64_t n, int64_t m, int64_t n_global, bd_csr* S1,
+                          bd_csr* Si, const double* mass, const double* heart_mass, double gamma,
+                          bd_inner* bulk, bd_inner* schur, double msum, int64_t hist_cap,
+                          double* red, bd_csr* Si_ext, double* z1ext, bd_shard** out);
+bd_status bd_shard_destroy(bd_shard* h);
+/* device pointers: {x, r, d, q, z1, s, red, z2, corr} (red: the caller's) */
+bd_status bd_shard_vectors(bd_shard* h, double** ptrs);
+bd_status bd_shard_begin(bd_shard* h, double tol, int64_t max_iter, const double* x0);
+bd_status bd_shard_lambda(bd_shard* h, const double* v, const double* ug, const double* vg,
+                          int use_flags);
+bd_status bd_shard_init(bd_shard* h, const double* b, int has_x0);
+bd_status bd_shard_check(bd_shard* h, int initial);
+bd_status bd_shard_update(bd_shard* h);
+bd_status bd_shard_pinv1(bd_shard* h);
+bd_status bd_shard_pinv2(bd_shard* h, const double* tg);
+bd_status bd_shard_pinv3(bd_shard* h, const double* sg);
+bd_status bd_shard_pinv4(bd_shard* h);
+bd_status bd_shard_finish(bd_shard* h, int initial);
+bd_status bd_shard_wmean(bd_shard* h);
+bd_status bd_shard_normalize(bd_shard* h, double* out);
+bd_status bd_shard_done(bd_shard* h, int* done);
+/* info = {iterations, converged, breakdown, zero_rhs, max_iter_hit, n_res,
+ * n_prec}; scal = {last relative residual, curvature}; histories host. */
+bd_status bd_shard_read(bd_shard* h, int64_t* info, double* scal, double* res_hist,
+                        double* prec_hist, int64_t cap);
+/* dst[i] = src[idx[i]] (device; halo packing) */
+bd_status bd_gather(bd_ctx* ctx, int64_t k, const int64_t* idx, const double* src, double* dst);
 
 #ifdef __cplusplus
 }

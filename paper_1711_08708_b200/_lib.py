@@ -88,6 +88,25 @@ SIGNATURES = [
     ("bd_tensors_transmural", _i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     ("bd_assemble_destroy", _i32, [_vp]),
     ("bd_step_track", _i32, [_vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _dbl, _dbl, _vp, C.POINTER(_dbl)]),
+    ("bd_shard_create", _i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _vp, _dbl,
+                               _i64, _vp, _vp, _vp, _pp]),
+    ("bd_shard_destroy", _i32, [_vp]),
+    ("bd_shard_vectors", _i32, [_vp, _pp]),
+    ("bd_shard_begin", _i32, [_vp, _dbl, _i64, _vp]),
+    ("bd_shard_lambda", _i32, [_vp, _vp, _vp, _vp, C.c_int]),
+    ("bd_shard_init", _i32, [_vp, _vp, C.c_int]),
+    ("bd_shard_check", _i32, [_vp, C.c_int]),
+    ("bd_shard_update", _i32, [_vp]),
+    ("bd_shard_pinv1", _i32, [_vp]),
+    ("bd_shard_pinv2", _i32, [_vp, _vp]),
+    ("bd_shard_pinv3", _i32, [_vp, _vp]),
+    ("bd_shard_pinv4", _i32, [_vp]),
+    ("bd_shard_finish", _i32, [_vp, C.c_int]),
+    ("bd_shard_wmean", _i32, [_vp]),
+    ("bd_shard_normalize", _i32, [_vp, _vp]),
+    ("bd_shard_done", _i32, [_vp, C.POINTER(C.c_int)]),
+    ("bd_shard_read", _i32, [_vp, C.POINTER(_i64), C.POINTER(_dbl), _vp, _vp, _i64]),
+    ("bd_gather", _i32, [_vp, _i64, _vp, _vp, _vp]),
 ]
 
 _lib = None

@@ -2026,10 +2026,16 @@ bd_status bd_spmv_split(bd_csr* a, const double* x, int64_t nsplit, const double
                         double* y, double alpha, double beta) {
   if (!a || !x || !y || nsplit < 0 || (nsplit < a->ncols && !x_ghost)) return BD_EINVAL;
   bd_ctx* ctx = a->ctx;
-  if (!a->ell_w) return fail(ctx, BD_EINVAL, "bd_spmv_split: matrix has no ELL copy (rows too long)");
   Scope sc(ctx);
   const int grid = grid_for(ctx, a->nrows, dev::TPB);
   const int ns = (int)std::min<int64_t>(nsplit, 0x7fffffff);
+  if (!a->ell_w) {  // irregular / small blocks: CSR rows, one thread each
+    if (a->nrows == 0) return BD_OK;
+    dev::k_spmv_csr_split<<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->rowptr, a->col, a->val, x,
+                                                              x_ghost, ns, y, alpha, beta);
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
   switch (a->ell_w) {
     case 8: dev::k_spmv_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns); break;
     case 16: dev::k_spmv_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(a->nrows, a->ell_col, a->ell_val, x, y, alpha, beta, x_ghost, ns); break;
@@ -2994,6 +3000,358 @@ bd_status bd_membrane_gate(bd_ctx* ctx, int64_t m, const double* v, const double
   Scope sc(ctx);
   dev::k_membrane_gate<<<grid_for(ctx, m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
       m, v, w, dt, v_rest, v_span, tau_open, tau_close, u_gate, w_new);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+
+}  // extern "C"
+
+// ---- sharded PCG iteration (one rank of distributed.py; bd_shard.cuh) -------------
+struct bd_shard {
+  bd_ctx* ctx = nullptr;
+  int64_t n = 0, m = 0, n_global = 0;
+  bd_csr *S1 = nullptr, *Si = nullptr;
+  bd_csr* Si_ext = nullptr;  // S_i with its ghost columns at n + j: reads [z1 | ghosts] in place
+  double* z1ext = nullptr;    // caller-owned: z1 (n) followed by its heart ghosts
+  double* zero_sc = nullptr;  // zero scalar slots (RhsSchur without recentring)
+  bd_inner *bulk = nullptr, *schur = nullptr;
+  double gamma = 0.0, msum = 1.0;
+  double *x = nullptr, *r = nullptr, *d = nullptr, *q = nullptr, *z1 = nullptr, *z2 = nullptr,
+         *s = nullptr, *rhs_s = nullptr, *corr = nullptr, *mh = nullptr, *mass = nullptr;
+  double *sc = nullptr, *red = nullptr, *part = nullptr, *res_hist = nullptr, *prec_hist = nullptr;
+  int *fl = nullptr, *si = nullptr;
+  unsigned* ctr = nullptr;
+  int hist_cap = 0;
+  Ctl cb{}, cs{};  // the inners' control blocks with the shard's done flag
+};
+
+namespace {
+__global__ void k_sh_begin(double* sc, int* fl, int* si, double tol, int64_t max_iter) {
+  for (int i = 0; i < dev::SH_NSLOTS; ++i) sc[i] = 0.0;
+  for (int i = 0; i < dev::NFLAGS; ++i) fl[i] = 0;
+  for (int i = 0; i < dev::SHI_NINT; ++i) si[i] = 0;
+  sc[dev::SH_TOL] = tol;
+  si[dev::SHI_MAXITER] = (int)max_iter;
+}
+
+template <class Rhs>
+bd_status shard_inner(bd_inner* p, const Rhs& rhs, double* z, const Ctl& c) {
+  if (p->kind == BD_INNER_JACOBI) return inner_solve(p, rhs, z, nullptr, c, dev::C_JAC1);
+  return inner_solve(p, rhs, p->x_int, z, c, dev::C_BULK1_S);
+}
+}  // namespace
+
+extern "C" {
+
+bd_status bd_shard_create(bd_ctx* ctx, int64_t n, int64_t m, int64_t n_global, bd_csr* S1,
+                          bd_csr* Si, const double* mass, const double* heart_mass, double gamma,
+                          bd_inner* bulk, bd_inner* schur, double msum, int64_t hist_cap,
+                          double* red, bd_csr* Si_ext, double* z1ext, bd_shard** out) {
+  if (!ctx || !S1 || !Si || !mass || !heart_mass || !bulk || !schur || !red || !out || n <= 0 || m < 0 ||
+      m > n || S1->nrows != n || Si->nrows != m || bulk->n != n || schur->n != m)
+    return fail(ctx, BD_EINVAL, "bd_shard_create: inconsistent arguments");
+  auto* h = new bd_shard();
+  h->ctx = ctx;
+  h->n = n;
+  h->m = m;
+  h->n_global = n_global;
+  h->S1 = S1;
+  h->Si = Si;
+  h->bulk = bulk;
+  h->schur = schur;
+  h->gamma = gamma;
+  h->msum = msum;
+  h->hist_cap = (int)std::max<int64_t>(hist_cap, 2);
+  h->red = red;  // caller-owned (the host all-reduces slices of it in place)
+  if (Si_ext && z1ext && Si_ext->nrows == m) {
+    h->Si_ext = Si_ext;
+    h->z1ext = z1ext;
+  }
+  const int64_t nm = n + m;
+  bool bad = dalloc(&h->x, nm) || dalloc(&h->r, nm) || dalloc(&h->d, nm) || dalloc(&h->q, nm) ||
+             (!h->z1ext && dalloc(&h->z1, n)) || dalloc(&h->z2, n) ||
+             dalloc(&h->zero_sc, dev::NSLOTS) || dalloc(&h->s, m) || dalloc(&h->rhs_s, m) ||
+             dalloc(&h->corr, n) || dalloc(&h->mh, m) || dalloc(&h->mass, n) ||
+             dalloc(&h->sc, dev::SH_NSLOTS) ||
+             dalloc(&h->part, (int64_t)dev::SH_GRID * 4) || dalloc(&h->res_hist, h->hist_cap) ||
+             dalloc(&h->prec_hist, h->hist_cap) || dalloc(&h->fl, dev::NFLAGS) ||
+             dalloc(&h->si, dev::SHI_NINT) || dalloc(&h->ctr, 8);
+  if (h->z1ext) h->z1 = h->z1ext;
+  bad = bad || cudaMemset(h->corr, 0, sizeof(double) * n) ||
+        cudaMemset(h->zero_sc, 0, sizeof(double) * dev::NSLOTS) || cudaMemset(h->d, 0, sizeof(double) * nm) ||
+        cudaMemset(h->red, 0, sizeof(double) * dev::SH_RED) || cudaMemset(h->ctr, 0, sizeof(unsigned) * 8) ||
+        cudaMemset(h->fl, 0, sizeof(int) * dev::NFLAGS) || cudaMemset(h->si, 0, sizeof(int) * dev::SHI_NINT) ||
+        cudaMemcpy(h->mh, heart_mass, sizeof(double) * m, cudaMemcpyHostToDevice) ||
+        cudaMemcpy(h->mass, mass, sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (bad) {
+    bd_shard_destroy(h);
+    return fail(ctx, BD_ECUDA, "bd_shard_create: device allocation failed");
+  }
+  h->cb = bulk->ctl;
+  h->cb.fl = h->fl;
+  h->cb.use_flags = 1;
+  h->cs = schur->ctl;
+  h->cs.fl = h->fl;
+  h->cs.use_flags = 1;
+  *out = h;
+  return BD_OK;
+}
+
+bd_status bd_shard_destroy(bd_shard* h) {
+  if (!h) return BD_OK;
+  for (double* p : {h->x, h->r, h->d, h->q, h->z2, h->s, h->rhs_s, h->corr, h->mh, h->mass,
+                    h->sc, h->part, h->res_hist, h->prec_hist, h->zero_sc})
+    cudaFree(p);
+  if (!h->z1ext) cudaFree(h->z1);
+  cudaFree(h->fl);
+  cudaFree(h->si);
+  cudaFree(h->ctr);
+  delete h;
+  return BD_OK;
+}
+
+bd_status bd_shard_vectors(bd_shard* h, double** ptrs) {
+  if (!h || !ptrs) return BD_EINVAL;
+  double* v[9] = {h->x, h->r, h->d, h->q, h->z1, h->s, h->red, h->z2, h->corr};
+  for (int i = 0; i < 9; ++i) ptrs[i] = v[i];
+  return BD_OK;
+}
+
+bd_status bd_shard_begin(bd_shard* h, double tol, int64_t max_iter, const double* x0) {
+  if (!h || !(tol > 0.0) || max_iter < 0) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  if (max_iter + 2 > h->hist_cap) return fail(ctx, BD_EINVAL, "bd_shard_begin: max_iter exceeds the history capacity");
+  Scope sc(ctx);
+  k_sh_begin<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->si, tol, max_iter);
+  LAUNCHED(ctx);
+  if (x0)
+    CK(ctx, cudaMemcpyAsync(h->x, x0, sizeof(double) * (h->n + h->m), cudaMemcpyDeviceToDevice, ctx->stream));
+  else
+    CK(ctx, cudaMemsetAsync(h->x, 0, sizeof(double) * (h->n + h->m), ctx->stream));
+  return BD_OK;
+}
+
+// q = Λ_local v with v's halo (ug: all ghosts, vg: heart ghosts); red[0] = v·q
+bd_status bd_shard_lambda(bd_shard* h, const double* v, const double* ug, const double* vg,
+                          int use_flags) {
+  if (!h || !v) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  const int64_t n = h->n, m = h->m;
+  if (h->S1->ell_w && (m == 0 || h->Si->ell_w) && !getenv("BD_SHARD_LAMBDA_SPLIT")) {
+    Scope sc(ctx);  // one fused pass (k_sh_lambda_ell)
+    dev::k_sh_lambda_ell<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(
+        n, m, h->S1->ell_w, h->S1->ell_col, h->S1->ell_val, m ? h->Si->ell_w : 0,
+        m ? h->Si->ell_col : nullptr, m ? h->Si->ell_val : nullptr, v, ug, vg, h->q, h->mh,
+        h->gamma, h->part, h->ctr + 0, h->red + 0, h->fl, use_flags);
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
+  TRY(bd_spmv_split(h->S1, v, n, ug, h->q, 1.0, 0.0));
+  if (m > 0) {
+    TRY(bd_spmv_split(h->Si, v + n, m, vg, h->q + n, 1.0, 0.0));  // S_i v
+    Scope sc(ctx);
+    dev::k_sh_lam_add<<<grid_for(ctx, m, dev::TPB), dev::TPB, 0, ctx->stream>>>(m, h->q, h->q + n,
+                                                                             h->fl, use_flags);
+    LAUNCHED(ctx);
+  }
+  if (m > 0) TRY(bd_spmv_split(h->Si, v, m, ug, h->q + n, 1.0, 1.0));  // S_i u_H + S_i v
+  Scope sc(ctx);
+  dev::k_sh_lam_fin<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(n, n + m, v, h->q, h->mh, h->gamma,
+                                                                h->part, h->ctr + 0, h->red + 0,
+                                                                h->fl, use_flags);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// r = b − Λx0 (q from bd_shard_lambda on x0) or b; red[1], red[2], red[7]
+bd_status bd_shard_init(bd_shard* h, const double* b, int has_x0) {
+  if (!h || !b) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_init<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->n + h->m, b, has_x0 ? h->q : nullptr,
+                                                             h->r, h->Si_ext ? nullptr : h->rhs_s,
+                                                             h->part, h->ctr + 1,
+                                                             h->red + 1);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_shard_check(bd_shard* h, int initial) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  if (initial) {  // k_sh_init wrote (‖r‖², Σr_u, ‖b‖²) to red[1..3]: move ‖b‖² to red[7]
+    CK(ctx, cudaMemcpyAsync(h->red + 7, h->red + 3, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  dev::k_sh_check<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->si, h->red, h->res_hist, h->hist_cap,
+                                            h->n_global, initial);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+bd_status bd_shard_update(bd_shard* h) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_alpha<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->si, h->red);
+  LAUNCHED(ctx);
+  dev::k_sh_update<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->n + h->m, h->x, h->r, h->d, h->q,
+                                                               h->Si_ext ? nullptr : h->rhs_s, h->sc,
+                                                               h->part, h->ctr + 2,
+                                                               h->red + 1, h->fl);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// z1 = bulk^{-1}(r_u − μ1)
+bd_status bd_shard_pinv1(bd_shard* h) {
+  if (!h) return BD_EINVAL;
+  Scope sc(h->ctx);
+  dev::RhsVec rhs{h->r, (int)h->n, h->sc + dev::SH_MU1, h->bulk->perm};
+  return shard_inner(h->bulk, rhs, h->z1, h->cb);
+}
+
+// s = K^{-1}(r_v − S_i [z1 | tg]); with S_i's ghost columns at n + j and the
+// halo received into z1ext[n..), the product is formed inside the Schur
+// forward pass (RhsSchur, as the single-GPU path) and tg is not read
+bd_status bd_shard_pinv2(bd_shard* h, const double* tg) {
+  if (!h) return BD_EINVAL;
+  if (h->m == 0) return BD_OK;
+  if (h->Si_ext) {
+    Scope sc(h->ctx);
+    dev::RhsSchur rhs{h->Si_ext->dev(), h->z1ext, h->zero_sc, h->r + h->n, h->schur->perm};
+    return shard_inner(h->schur, rhs, h->s, h->cs);
+  }
+  TRY(bd_spmv_split(h->Si, h->z1, h->m, tg, h->rhs_s, -1.0, 1.0));
+  Scope sc(h->ctx);
+  dev::RhsVec rhs{h->rhs_s, (int)h->m, nullptr, h->schur->perm};
+  return shard_inner(h->schur, rhs, h->s, h->cs);
+}
+
+// corr = pad(S_i [s | sg]); red[3] = Σ corr
+bd_status bd_shard_pinv3(bd_shard* h, const double* sg) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  if (h->m > 0 && h->Si->ell_w) {  // one pass: product and its sum
+    Scope sc(ctx);
+    dev::k_sh_corr_ell<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(
+        h->m, h->Si->ell_w, h->Si->ell_col, h->Si->ell_val, h->s, sg, h->corr, h->part, h->ctr + 3,
+        h->red + 3, h->fl);
+    LAUNCHED(ctx);
+    return BD_OK;
+  }
+  if (h->m > 0) TRY(bd_spmv_split(h->Si, h->s, h->m, sg, h->corr, 1.0, 0.0));
+  Scope sc(ctx);
+  dev::k_sh_sum<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->m, h->corr, h->part, h->ctr + 3,
+                                                            h->red + 3, h->fl);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// z2 = bulk^{-1}(corr − μ2); w = z1 − z2; red[4..6] = Σw, r_u·w, r_v·s
+bd_status bd_shard_pinv4(bd_shard* h) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_mu2<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->red, h->n_global);
+  LAUNCHED(ctx);
+  dev::RhsVec rhs{h->corr, (int)h->n, h->sc + dev::SH_MU2, h->bulk->perm};
+  TRY(shard_inner(h->bulk, rhs, h->z2, h->cb));
+  dev::k_sh_combine<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->m, h->z1, h->z2, h->r, h->s,
+                                                                h->part, h->ctr + 4, h->red + 4, h->fl);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// ρ_next, β; d = z + βd (initial: d = z)
+bd_status bd_shard_finish(bd_shard* h, int initial) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_finish<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->si, h->red, h->prec_hist, h->hist_cap,
+                                             h->n_global, initial);
+  LAUNCHED(ctx);
+  if (initial) CK(ctx, cudaMemsetAsync(h->d, 0, sizeof(double) * (h->n + h->m), ctx->stream));
+  dev::k_sh_dupdate<<<grid_for(ctx, h->n + h->m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      h->n, h->m, h->z1, h->s, h->d, h->sc, h->fl);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// red[8] = Σ mass ∘ x_u (the weighted mean's numerator, before its all-reduce)
+bd_status bd_shard_wmean(bd_shard* h) {
+  if (!h) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_wmean<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->mass, h->x, h->part, h->ctr + 5,
+                                                              h->red + 8);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// out = normalize(x) with the all-reduced red[8] (zero for a zero rhs)
+bd_status bd_shard_normalize(bd_shard* h, double* out) {
+  if (!h || !out) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  dev::k_sh_normalize<<<grid_for(ctx, h->n + h->m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+      h->n, h->n + h->m, h->x, out, h->red, h->msum, h->si);
+  LAUNCHED(ctx);
+  return BD_OK;
+}
+
+// done flag only (the host's periodic loop test); synchronising
+bd_status bd_shard_done(bd_shard* h, int* done) {
+  if (!h || !done) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  int* hp = (int*)(ctx->h_pin + 40);
+  CK(ctx, cudaMemcpyAsync(hp, h->fl + dev::F_DONE, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  *done = hp[0];
+  return BD_OK;
+}
+
+// info = {iterations, converged, breakdown, zero_rhs, max_iter_hit, n_res, n_prec};
+// scal = {last relative residual, curvature at a breakdown}; histories: host
+// arrays of capacity cap (may be NULL).  Synchronising.
+bd_status bd_shard_read(bd_shard* h, int64_t* info, double* scal, double* res_hist,
+                        double* prec_hist, int64_t cap) {
+  if (!h || !info) return BD_EINVAL;
+  bd_ctx* ctx = h->ctx;
+  Scope sc(ctx);
+  int si[dev::SHI_NINT];
+  double s[dev::SH_NSLOTS];
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemcpy(si, h->si, sizeof(si), cudaMemcpyDeviceToHost));
+  CK(ctx, cudaMemcpy(s, h->sc, sizeof(s), cudaMemcpyDeviceToHost));
+  info[0] = si[dev::SHI_ITERS];
+  info[1] = si[dev::SHI_CONV];
+  info[2] = si[dev::SHI_BAD];
+  info[3] = si[dev::SHI_ZERO];
+  info[4] = si[dev::SHI_MAXIT];
+  info[5] = std::min(si[dev::SHI_NRES], h->hist_cap);
+  info[6] = std::min(si[dev::SHI_NPREC], h->hist_cap);
+  if (scal) {
+    scal[0] = s[dev::SH_REL];
+    scal[1] = s[dev::SH_CURV];
+  }
+  if (res_hist && info[5])
+    CK(ctx, cudaMemcpy(res_hist, h->res_hist, sizeof(double) * std::min<int64_t>(info[5], cap),
+                       cudaMemcpyDeviceToHost));
+  if (prec_hist && info[6])
+    CK(ctx, cudaMemcpy(prec_hist, h->prec_hist, sizeof(double) * std::min<int64_t>(info[6], cap),
+                       cudaMemcpyDeviceToHost));
+  return BD_OK;
+}
+
+// dst[i] = src[idx[i]] (device; halo packing)
+bd_status bd_gather(bd_ctx* ctx, int64_t k, const int64_t* idx, const double* src, double* dst) {
+  if (!ctx || k < 0 || (k && (!idx || !src || !dst))) return BD_EINVAL;
+  if (k == 0) return BD_OK;
+  Scope sc(ctx);
+  dev::k_sh_gather<<<grid_for(ctx, k, dev::TPB), dev::TPB, 0, ctx->stream>>>(k, idx, src, dst);
   LAUNCHED(ctx);
   return BD_OK;
 }

@@ -662,3 +662,4 @@ struct RhsSchur {
 
 #include "bd_trsv.cuh"
 #include "bd_vec.cuh"
+#include "bd_shard.cuh"

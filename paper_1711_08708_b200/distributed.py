@@ -16,11 +16,14 @@ block-LU preconditioner (bd/precond.py:281-312), with two changes:
   preconditioner, so their iteration counts are reported next to the
   1-GPU counts.
 
-Local compute goes through a backend object.  ``NativeBackend`` runs SpMV and
-the inner solves in the sm_100a library.  The CPU tests inject a scipy backend
-(tests/test_distributed.py) to check the partition / halo / collective logic
-with gloo at world size 2.  Vectors are torch tensors on the rank's device;
-collectives are torch.distributed (NCCL over NVLink on the box).
+The rank-local iteration is native: ``NativeShard`` holds the rank's PCG
+state and runs every vector operation, the local Λ and the block-Jacobi inner
+solves as sm_100a kernels (bd_shard_*, csrc/bd_shard.cuh) with all scalars on
+the device.  ``ShardSolver`` interleaves them with three halo exchanges and
+four all-reduces per iteration (torch.distributed: NCCL over NVLink on the
+box) and captures one iteration, collectives included, in a CUDA graph.
+``TorchShard`` restates the same kernels on CPU tensors so the CPU tests run
+the identical orchestration with gloo at world size 2.
 """
 from __future__ import annotations
 
@@ -96,8 +99,7 @@ def build_local(S1, Si, mass, heart_mass, gamma, grounded, Km, part: np.ndarray,
         own = np.concatenate([own[own < m], own[own >= m]])
         rows = S1[own]
         cols = np.unique(rows.indices)
-        gh = cols[part[cols] != r]
-        gh = np.concatenate([gh[gh < m], gh[gh >= m]])
+        gh = order_ghosts(cols[part[cols] != r], m, part)
         return own, gh
 
     lay = [layout(r) for r in range(nprocs)]
@@ -142,16 +144,13 @@ def build_local(S1, Si, mass, heart_mass, gamma, grounded, Km, part: np.ndarray,
 
 # ---- communication -------------------------------------------------------------------
 class Comm:
-    """torch.distributed wrapper: halo exchange and global sums.
-
-    Nothing here reads a value back to the host: sums are all-reduced in place
-    on device tensors (NCCL on the box, gloo in the CPU tests) and the halo
-    index lists are uploaded once."""
+    """torch.distributed wrapper: in-place global sums of device tensors and
+    point-to-point halo messages (NCCL on the box, gloo in the CPU tests).
+    Nothing here reads a value back to the host."""
 
     def __init__(self, dist, device):
         self.dist = dist
         self.device = device
-        self._idx = {}
         # one rank: every sum is already global (no collective in the loop)
         self.single = dist.get_world_size() == 1
 
@@ -170,31 +169,14 @@ class Comm:
             self.dist.all_reduce(t)
         return t
 
-    def _index(self, key, idx):
-        torch = _torch()
-        t = self._idx.get(key)
-        if t is None:
-            t = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=self.device)
-            self._idx[key] = t
-        return t
-
-    def halo(self, x_own, send: dict, recv: dict, nslots: int, tag: str = ""):
-        """Ghost values of x from the owning neighbours (one layer)."""
-        torch = _torch()
-        out = torch.zeros(nslots, dtype=x_own.dtype, device=x_own.device)
-        ops, bufs = [], {}
-        for q, idx in send.items():
-            buf = x_own.index_select(0, self._index((tag, "s", q), idx))
-            ops.append(self.dist.P2POp(self.dist.isend, buf, q))
-        for q, slots in recv.items():
-            bufs[q] = torch.empty(len(slots), dtype=x_own.dtype, device=x_own.device)
-            ops.append(self.dist.P2POp(self.dist.irecv, bufs[q], q))
+    def exchange(self, sends, recvs):
+        """sends / recvs: lists of (peer, contiguous tensor view), matched per
+        peer in list order (zero-length messages are left out on both sides)."""
+        ops = [self.dist.P2POp(self.dist.isend, buf, q) for q, buf in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, buf, q) for q, buf in recvs]
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
-        for q, slots in recv.items():
-            out.index_copy_(0, self._index((tag, "r", q), slots), bufs[q])
-        return out
 
 
 def _torch():
@@ -203,289 +185,564 @@ def _torch():
     return torch
 
 
-# ---- distributed operator and solver ----------------------------------------------------
-class DistributedSystem:
-    """Λ on the rank's owned rows (block vector = [u_own | v_own])."""
+def order_ghosts(g: np.ndarray, m: int, part: np.ndarray) -> np.ndarray:
+    """Ghost order of a rank: heart ghosts, then torso ghosts, each grouped by
+    owning rank (ascending) and ascending within a group, so every
+    neighbour's ghosts are one contiguous heart range and one contiguous
+    torso range (halos land in place, no scatter)."""
+    g = np.asarray(g, dtype=np.int64)
+    out = []
+    for blk in (g[g < m], g[g >= m]):
+        out.append(blk[np.lexsort((blk, part[blk]))])
+    return np.concatenate(out)
 
-    def __init__(self, lp: LocalProblem, comm: Comm, backend):
-        self.lp, self.comm, self.be = lp, comm, backend
-        self.S1 = backend.matrix(lp.S1)
-        self.Si = backend.matrix(lp.Si)
+
+class HaloPlan:
+    """Per-neighbour message layout of the three halos of an iteration: the
+    search direction d = [u | v] (all ghosts of u, heart ghosts of v) before
+    Λ, and the heart ghosts of z1 (for S_i t) and of s (for S_i s) in P^{-1}.
+    Send side: one packed buffer gathered by one kernel (bd_gather); receive
+    side: contiguous ranges of the ghost buffers (order_ghosts)."""
+
+    def __init__(self, lp: "LocalProblem", device, gather):
         torch = _torch()
-        self.mh = torch.as_tensor(lp.heart_mass, device=comm.device)
-        self.mass = torch.as_tensor(lp.mass, device=comm.device)
-        self.msum = comm.allreduce([float(lp.mass.sum())])[0]
-
-    @property
-    def n(self):
-        return self.lp.n_own
-
-    @property
-    def m(self):
-        return self.lp.m_own
-
-    def heart_ghosts(self, v):
-        lp = self.lp
-        return self.comm.halo(v, lp.send_heart, lp.recv_heart, lp.m_ghost, "h")
-
-    def spmv_split(self, a, x, nsplit, x_ghost, out=None):
-        """a @ [x[:nsplit] ; x_ghost] without concatenating (native backend:
-        bd_spmv_split); backends without it (the CPU test double) concatenate."""
-        f = getattr(self.be, "spmv_split", None)
-        if f is not None:
-            return f(a, x, nsplit, x_ghost, out)
-        y = self.be.spmv(a, _torch().cat([x[:nsplit], x_ghost]))
-        if out is None:
-            return y
-        out.copy_(y)
-        return out
-
-    def apply(self, x):
-        """q = Λ x (bd/system.py:106-116) with halo exchanges of u and v.
-        Local columns are [owned | ghosts] for S_1 and [owned heart | ghost
-        heart] for S_i; heart vertices lead both the owned and the ghost lists,
-        so the S_i products read u and v with a split at m_own."""
-        lp = self.lp
         n, m = lp.n_own, lp.m_own
-        u, v = x[:n], x[n:]
-        ug = self.comm.halo(u, lp.send, lp.recv, lp.ghosts.size, "u")
-        vg = self.heart_ghosts(v)
-        q = _torch().empty_like(x)
-        iv = self.spmv_split(self.Si, v, m, vg)
-        self.spmv_split(self.S1, u, n, ug, out=q[:n])
-        q[:m] += iv
-        qv = q[n:]
-        self.spmv_split(self.Si, u, m, ug, out=qv)
-        qv += iv
-        qv += lp.gamma * (self.mh * v)
-        return q
+        gh = lp.ghosts
+        self.n_ghost, self.m_ghost = gh.size, lp.m_ghost
+        self.gather = gather
+        self.peers = sorted(set(lp.send) | set(lp.recv))
+        d_idx, h_idx = [], []
+        self.d_send, self.h_send = [], []  # (peer, offset, [lengths])
+        off_d = off_h = 0
+        for q in self.peers:
+            snd = np.asarray(lp.send.get(q, np.zeros(0, np.int64)), dtype=np.int64)
+            nh = int((snd < m).sum())
+            assert (snd[:nh] < m).all() and (snd[nh:] >= m).all(), "heart-first send order"
+            d_idx += [snd[:nh], snd[nh:], snd[:nh] + n]
+            h_idx.append(snd[:nh])
+            self.d_send.append((q, off_d, [nh, snd.size - nh, nh]))
+            self.h_send.append((q, off_h, [nh]))
+            off_d += snd.size + nh
+            off_h += nh
+        cat = lambda a: torch.as_tensor(np.concatenate(a) if a else np.zeros(0, np.int64),  # noqa: E731
+                                        dtype=torch.int64, device=device)
+        self.d_idx, self.h_idx = cat(d_idx), cat(h_idx)
+        self.d_buf = torch.zeros(max(off_d, 1), dtype=torch.float64, device=device)
+        self.h_buf = torch.zeros(max(off_h, 1), dtype=torch.float64, device=device)
+        # receive ranges: heart [h0, h1) and torso [t0, t1) of the ghost list
+        self.recv = {}
+        for q in self.peers:
+            slots = np.asarray(lp.recv.get(q, np.zeros(0, np.int64)), dtype=np.int64)
+            hs, ts = slots[slots < lp.m_ghost], slots[slots >= lp.m_ghost]
+            for s in (hs, ts):
+                assert s.size == 0 or np.array_equal(s, np.arange(s[0], s[0] + s.size)), \
+                    "ghosts not grouped by owner"
+            self.recv[q] = ((int(hs[0]) if hs.size else 0, hs.size),
+                            (int(ts[0]) if ts.size else 0, ts.size))
+        self.ug = torch.zeros(max(self.n_ghost, 1), dtype=torch.float64, device=device)
+        self.vg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
+        self.tg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
+        self.sg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
 
-    def dot_t(self, a, b):
-        """Global a·b as a device 0-d tensor (one fused dot per rank)."""
-        return self.comm.allreduce_(_torch().dot(a, b).reshape(1))[0]
+    def halo_d(self, comm, src):
+        """ug, vg <- ghosts of u and heart ghosts of v of the block vector src."""
+        if not self.peers:
+            return
+        self.gather(self.d_idx, src, self.d_buf)
+        sends, recvs = [], []
+        for q, off, lens in self.d_send:
+            for ln in lens:
+                if ln:
+                    sends.append((q, self.d_buf[off: off + ln]))
+                off += ln
+        for q in self.peers:
+            (h0, hn), (t0, tn) = self.recv[q]
+            if hn:
+                recvs.append((q, self.ug[h0: h0 + hn]))
+            if tn:
+                recvs.append((q, self.ug[t0: t0 + tn]))
+            if hn:
+                recvs.append((q, self.vg[h0: h0 + hn]))
+        comm.exchange(sends, recvs)
 
-    def mean_u_t(self, u):
-        return self.comm.allreduce_(u.sum().reshape(1))[0] / self.lp.n_global
-
-    def dot(self, a, b):
-        return float(self.dot_t(a, b))
-
-    def mean_u(self, u):
-        return float(self.mean_u_t(u))
-
-    def normalize(self, x):
-        lp = self.lp
-        alpha = self.comm.allreduce_((self.mass * x[: lp.n_own]).sum().reshape(1))[0] / self.msum
-        out = x.clone()
-        out[: lp.n_own] -= alpha
-        return out
-
-
-class DistributedBlockLU:
-    """Block-LU P_Λ (bd/precond.py:281-312) with block-Jacobi inner solves."""
-
-    def __init__(self, dsys: DistributedSystem, inner: str, beta: float):
-        self.s, self.beta = dsys, beta
-        be = dsys.be
-        lp = dsys.lp
-        xyz = getattr(lp, "coords", None)  # owned-vertex coordinates: lattice tiles for IC(0)
-        self.bulk = be.inner(inner, lp.bulk_block, None if xyz is None else xyz)
-        self.schur = be.inner(inner, lp.schur_block, None if xyz is None else xyz[: lp.m_own])
-        self.p1 = self.pk = self.si = 0
-        self._corr = None  # pad(S_i s): torso rows stay zero, heart rows rewritten per apply
-
-    def bulk_inverse(self, y, mean=None):
-        """`mean` (device 0-d): mean(y) when the caller already reduced it."""
-        self.p1 += 1
-        s = self.s
-        if mean is None:
-            mean = s.mean_u_t(y)
-        z = s.be.inner_apply(self.bulk, y - mean)
-        z = z - s.mean_u_t(z)
-        return z + mean / self.beta
-
-    def apply(self, r, mean_ru=None):
-        s, lp = self.s, self.s.lp
-        ru, rv = r[: lp.n_own], r[lp.n_own:]
-        t = self.bulk_inverse(ru, mean_ru)
-        tg = s.heart_ghosts(t[: lp.m_own])  # collective on all ranks
-        self.si += 1
-        self.pk += 1
-        sv = s.be.inner_apply(self.schur, rv - s.spmv_split(s.Si, t, lp.m_own, tg))
-        sg = s.heart_ghosts(sv)
-        self.si += 1
-        if self._corr is None or self._corr.shape != ru.shape or self._corr.device != ru.device:
-            self._corr = _torch().zeros_like(ru)
-        corr = self._corr
-        s.spmv_split(s.Si, sv, lp.m_own, sg, out=corr[: lp.m_own])
-        u = t - self.bulk_inverse(corr)
-        return _torch().cat([u, sv])
+    def halo_h(self, comm, src, dst):
+        """dst <- heart ghosts of the heart-block vector src."""
+        if not self.peers:
+            return
+        self.gather(self.h_idx, src, self.h_buf)
+        sends = [(q, self.h_buf[off: off + lens[0]]) for q, off, lens in self.h_send if lens[0]]
+        recvs = [(q, dst[h0: h0 + hn]) for q in self.peers for (h0, hn), _ in [self.recv[q]] if hn]
+        comm.exchange(sends, recvs)
 
 
-def distributed_pcg(dsys: DistributedSystem, prec: DistributedBlockLU, b, tol=1e-6,
-                    max_iter=500, x0=None, check_every=16, graph=None):
-    """The reference iteration (bd/krylov.py:46-140) on the sharded system,
-    device-resident: every scalar (α, β, ρ, the means, the residual) stays a
-    device tensor, reductions are in-place all-reduces, and the host reads the
-    convergence / breakdown flags only every `check_every` iterations.
-    Iterations after convergence are masked to exact no-ops (α = 0, ρ and d
-    kept), so iterates, histories and counts equal those of the per-iteration
-    test.  On a CUDA device one iteration is captured into a CUDA graph (NCCL
-    collectives included) and replayed; `graph=False` (or a failed capture)
-    runs the same body eagerly.  Returns (x_local, stats dict); raises
-    RuntimeError past max_iter / on breakdown (bd/krylov.py:103-108, 133-135)."""
-    torch = _torch()
-    st = {"iterations": 0, "residual_history": [], "preconditioned_history": [],
-          "mv_count": 0, "converged": False}
-    n = dsys.n
-    nb = float(dsys.dot_t(b, b)) ** 0.5
-    if nb == 0.0:
-        st["residual_history"].append(0.0)
-        st["converged"] = True
-        return torch.zeros_like(b), st
-    if x0 is None:
-        x = torch.zeros_like(b)
-        r = b.clone()
-    else:
-        x = x0.clone()
-        r = b - dsys.apply(x)
-    st["mv_count"] += 1
-    rel = float(dsys.dot_t(r, r)) ** 0.5 / nb
-    st["residual_history"].append(rel)
-    if rel <= tol:
-        st["converged"] = True
-        return dsys.normalize(x), st
+# ---- the rank-local iteration: native (sm_100a) and a CPU restatement ----------------
+class NativeShard:
+    """One rank's PCG state and vector kernels in the sm_100a library
+    (bd_shard_*, csrc/bd_shard.cuh): Λ on the local rows, the x/r update, the
+    block-Jacobi P^{-1} with the collapsed recentrings, r·z, d; every scalar
+    on the device, partial sums in the caller-visible buffer `red`."""
 
-    def precond(r, mean_ru=None):
-        z = prec.apply(r, mean_ru)
-        z[:n] -= dsys.mean_u_t(z[:n])  # _deflate
-        return z
+    def __init__(self, lp: "LocalProblem", inner: str, ctx=None):
+        import ctypes as C
 
-    dev, f64 = b.device, torch.float64
-    cnt = [prec.p1, prec.pk, prec.si]
-    z = precond(r)
-    S = {  # static state of the loop (graph-safe: only updated in place)
-        "x": x, "r": r, "d": z.clone(),
-        "rho": dsys.dot_t(r, z).reshape(()).clone(),
-        "active": torch.ones((), dtype=torch.bool, device=dev),
-        "bad": torch.zeros((), dtype=torch.bool, device=dev),
-        "iters": torch.zeros((), dtype=torch.int64, device=dev),
-        "k": torch.zeros((), dtype=torch.int64, device=dev),
-        "res": torch.full((max_iter + 1,), -1.0, dtype=f64, device=dev),
-        "pre": torch.full((max_iter + 1,), float("nan"), dtype=f64, device=dev),
-    }
-    S["pre"][0] = S["rho"]
-    zero = torch.zeros((), dtype=f64, device=dev)
-
-    def body():
-        d, rho, active = S["d"], S["rho"], S["active"]
-        q = dsys.apply(d)
-        dq = dsys.dot_t(d, q)
-        brk = active & ~(torch.isfinite(dq) & (dq > 0))
-        S["bad"].logical_or_(brk)
-        go = active & ~brk
-        alpha = torch.where(go, rho / dq, zero)
-        S["x"].addcmul_(d, alpha)
-        S["r"].addcmul_(q, alpha, value=-1.0)
-        S["iters"].add_(go.to(torch.int64))
-        # ‖r‖² and Σ r_u (the first bulk solve's mean) in one all-reduce
-        pair = torch.stack([torch.dot(S["r"], S["r"]), S["r"][:n].sum()])
-        dsys.comm.allreduce_(pair)
-        relk = torch.sqrt(pair[0]) / nb
-        S["k"].add_(1)
-        S["res"].index_put_((S["k"],), torch.where(go, relk, torch.full_like(relk, -1.0)))
-        act = go & ~(relk <= tol)
-        zz = precond(S["r"], pair[1] / dsys.lp.n_global)
-        rho_next = dsys.dot_t(S["r"], zz)
-        S["pre"].index_put_((S["k"],), torch.where(act, rho_next, torch.full_like(rho_next, float("nan"))))
-        beta = torch.where(act, rho_next / rho, zero)
-        d.copy_(torch.where(act, zz + beta * d, d))
-        rho.copy_(torch.where(act, rho_next, rho))
-        active.copy_(act)
-
-    use_graph = graph if graph is not None else (dev.type == "cuda" and os.environ.get("BD_SHARDED_GRAPH", "1") != "0")
-    g = None
-    k_done = 0
-    if use_graph:
         from . import _lib
-        ctx = _lib.Context.default()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):  # first iteration eagerly: warms the allocator pools
-            ctx.sync_stream()
-            body()
-        torch.cuda.current_stream(dev).wait_stream(side)
-        k_done = 1
-        try:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                ctx.sync_stream()
-                body()
-        except Exception as e:  # capture unsupported here (e.g. P2P in capture): eager body
-            g = None
-            st["graph_error"] = f"{type(e).__name__}: {e}"[:300]
-        ctx.sync_stream()
-    while k_done < max_iter:
-        if g is not None:
-            g.replay()
-        else:
-            body()
-        k_done += 1
-        if k_done % check_every == 0 or k_done == max_iter:
-            if not bool(S["active"]) or bool(S["bad"]):
-                break
-    n_it = int(S["iters"])
-    # the reference applies P^-1 once before the loop and once per
-    # non-final iteration (bd/krylov.py:95, 125): p1 += 2, pk += 1, si += 2 each
-    prec.p1, prec.pk, prec.si = cnt[0] + 2 * n_it, cnt[1] + n_it, cnt[2] + 2 * n_it
-    bad = bool(S["bad"])
-    res = S["res"][1: k_done + 1].tolist()
-    st["residual_history"].extend(h for h in res if h >= 0)
-    pre = S["pre"][: k_done + 1].tolist()
-    st["preconditioned_history"] = [h for h in pre if h == h]
-    st["iterations"] = n_it
-    st["graph"] = g is not None
-    st["mv_count"] += n_it + (1 if bad else 0)
-    if bad:
-        raise RuntimeError("conjugate gradient breakdown: curvature <= 0 or not finite")
-    if bool(S["active"]):
-        raise RuntimeError(f"PCG did not reach tol={tol} within {max_iter} iterations")
-    st["converged"] = True
-    return dsys.normalize(S["x"]), st
-
-
-class NativeBackend:
-    """Local compute in the sm_100a library (SpMV, inner solves)."""
-
-    def __init__(self):
-        from . import _lib
+        from .precond import make_inner
         from .system import NativeCsr
 
-        self._lib = _lib
-        self._csr = NativeCsr
-        self.ctx = _lib.Context.default()
-
-    def matrix(self, a):
-        return self._csr(self.ctx, sp.csr_matrix(a))
-
-    def spmv(self, h, x):
-        return h.matvec(x.contiguous())
-
-    def spmv_split(self, h, x, nsplit, x_ghost, out=None):
-        return h.matvec_split(x.contiguous(), nsplit, x_ghost.contiguous(), y=out)
-
-    def inner(self, kind, a, coords=None):
-        from .precond import make_inner
-
-        p = make_inner(kind)
-        if coords is not None and hasattr(p, "setup") and kind == "ic0":
-            p.setup(a, coords=coords)
+        torch = _torch()
+        self._lib, self.C = _lib, C
+        self.ctx = ctx or _lib.Context.default()
+        self.device = self.ctx.device
+        self.lp = lp
+        self.n, self.m = lp.n_own, lp.m_own
+        self.S1 = NativeCsr(self.ctx, sp.csr_matrix(lp.S1))
+        self.Si = NativeCsr(self.ctx, sp.csr_matrix(lp.Si))
+        # S_i with ghost column j at n + j: reads [z1 (n) | heart ghosts] in place,
+        # so r_v − S_i t is formed inside the Schur forward pass (RhsSchur)
+        si = sp.csr_matrix(lp.Si)
+        col = si.indices.astype(np.int64)
+        col = np.where(col >= lp.m_own, col + (lp.n_own - lp.m_own), col)
+        self.Si_ext = NativeCsr(self.ctx, sp.csr_matrix((si.data, col, si.indptr),
+                                                        shape=(lp.m_own, lp.n_own + lp.m_ghost)))
+        self.z1ext = torch.zeros(lp.n_own + max(lp.m_ghost, 1), dtype=torch.float64,
+                                 device=self.device)
+        xyz = getattr(lp, "coords", None)
+        self.bulk = make_inner(inner)
+        self.schur = make_inner(inner)
+        if inner == "ic0" and xyz is not None:
+            self.bulk.setup(lp.bulk_block, coords=xyz)
+            self.schur.setup(lp.schur_block, coords=xyz[: lp.m_own])
         else:
-            p.setup(a)
-        return p
+            self.bulk.setup(lp.bulk_block)
+            self.schur.setup(lp.schur_block)
+        self.red = torch.zeros(16, dtype=torch.float64, device=self.device)
+        self.hist_cap = 0
+        self.h = None
+        self.msum = None
 
-    def inner_apply(self, h, y):
-        return h.apply_inverse(y.contiguous())
+    def create(self, msum: float, hist_cap: int):
+        C, L = self.C, self._lib
+        if self.h is not None and hist_cap <= self.hist_cap:
+            return
+        self.destroy()
+        h = C.c_void_p()
+        mass = np.ascontiguousarray(self.lp.mass, dtype=np.float64)
+        mh = np.ascontiguousarray(self.lp.heart_mass, dtype=np.float64)
+        L.check(L.lib().bd_shard_create(
+            self.ctx.handle, self.n, self.m, self.lp.n_global, self.S1.handle, self.Si.handle,
+            mass.ctypes.data, mh.ctypes.data, float(self.lp.gamma), self.bulk.handle,
+            self.schur.handle, float(msum), int(hist_cap), L.ptr(self.red), self.Si_ext.handle,
+            L.ptr(self.z1ext), C.byref(h)),
+            self.ctx.handle)
+        self.h, self.hist_cap, self.msum = h, hist_cap, msum
+        ptrs = (C.c_void_p * 9)()
+        L.check(L.lib().bd_shard_vectors(h, ptrs), self.ctx.handle)
+        self.ptr = {k: C.c_void_p(ptrs[i]) for i, k in enumerate(
+            ("x", "r", "d", "q", "z1", "s", "red", "z2", "corr"))}
+
+    def destroy(self):
+        if self.h is not None and self._lib._lib is not None:
+            self._lib._lib.bd_shard_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def _c(self, st):
+        self._lib.check(st, self.ctx.handle)
+
+    def sync(self):
+        """Run on torch's current stream (graph capture, torch ordering)."""
+        self.ctx.sync_stream()
+
+    # the kernels (see include/bidomain_b200.h, bd_shard_*)
+    def gather(self, idx, src, dst):
+        L = self._lib
+        self._c(L.lib().bd_gather(self.ctx.handle, int(idx.numel()), L.ptr(idx),
+                                  src if isinstance(src, self.C.c_void_p) else L.ptr(src),
+                                  L.ptr(dst)))
+
+    def begin(self, tol, max_iter, x0):
+        self._c(self._lib.lib().bd_shard_begin(self.h, float(tol), int(max_iter),
+                                               self._lib.ptr(x0)))
+
+    def lambda_(self, which, ug, vg, use_flags):
+        L = self._lib
+        self._c(L.lib().bd_shard_lambda(self.h, self.ptr[which], L.ptr(ug), L.ptr(vg),
+                                        int(use_flags)))
+
+    def init(self, b, has_x0):
+        self._c(self._lib.lib().bd_shard_init(self.h, self._lib.ptr(b), int(has_x0)))
+
+    def check(self, initial):
+        self._c(self._lib.lib().bd_shard_check(self.h, int(initial)))
+
+    def update(self):
+        self._c(self._lib.lib().bd_shard_update(self.h))
+
+    def pinv1(self):
+        self._c(self._lib.lib().bd_shard_pinv1(self.h))
+
+    def pinv2(self, tg):
+        self._c(self._lib.lib().bd_shard_pinv2(self.h, self._lib.ptr(tg)))
+
+    def pinv3(self, sg):
+        self._c(self._lib.lib().bd_shard_pinv3(self.h, self._lib.ptr(sg)))
+
+    def pinv4(self):
+        self._c(self._lib.lib().bd_shard_pinv4(self.h))
+
+    def finish(self, initial):
+        self._c(self._lib.lib().bd_shard_finish(self.h, int(initial)))
+
+    def wmean(self):
+        self._c(self._lib.lib().bd_shard_wmean(self.h))
+
+    def normalize(self, out):
+        self._c(self._lib.lib().bd_shard_normalize(self.h, self._lib.ptr(out)))
+
+    def done(self):
+        d = self.C.c_int()
+        self._c(self._lib.lib().bd_shard_done(self.h, self.C.byref(d)))
+        return bool(d.value)
+
+    def read(self, cap):
+        C = self.C
+        info = (C.c_int64 * 7)()
+        scal = (C.c_double * 2)()
+        res = np.zeros(cap)
+        pre = np.zeros(cap)
+        self._c(self._lib.lib().bd_shard_read(self.h, info, scal, res.ctypes.data,
+                                              pre.ctypes.data, cap))
+        return {"iterations": int(info[0]), "converged": bool(info[1]), "breakdown": bool(info[2]),
+                "zero_rhs": bool(info[3]), "max_iter": bool(info[4]),
+                "residual_history": res[: info[5]].tolist(),
+                "preconditioned_history": pre[: info[6]].tolist(), "curvature": float(scal[1])}
+
+    def tg_buffer(self, plan):
+        """Where the halo of z1 lands: right after z1 in z1ext."""
+        return self.z1ext[self.n: self.n + max(plan.m_ghost, 1)]
+
+    def factor_nnz(self):
+        try:
+            return int(self.bulk.factor_info()["nnz"]), int(self.schur.factor_info()["nnz"])
+        except Exception:  # jacobi
+            return 0, 0
+
+
+class TorchShard:
+    """CPU restatement of NativeShard's kernels (same arithmetic order, same
+    reduction slots, the same done-flag semantics) on torch CPU tensors with
+    caller-supplied inner solves: it lets the CPU tests run the sharded
+    orchestration (ShardSolver: halo plan, the four all-reduces, the loop)
+    with gloo at world size > 1.  Test infrastructure, not a product path."""
+
+    def __init__(self, lp: "LocalProblem", inner_factory):
+        torch = _torch()
+        self.lp = lp
+        self.n, self.m = lp.n_own, lp.m_own
+        self.S1, self.Si = sp.csr_matrix(lp.S1), sp.csr_matrix(lp.Si)
+        self.bulk = inner_factory(lp.bulk_block)
+        self.schur = inner_factory(lp.schur_block)
+        nm = self.n + self.m
+        f64 = torch.float64
+        self.v = {k: torch.zeros(nm, dtype=f64) for k in ("x", "r", "d", "q")}
+        self.v.update({k: torch.zeros(self.n, dtype=f64) for k in ("z1", "z2", "corr")})
+        self.v.update({k: torch.zeros(self.m, dtype=f64) for k in ("s", "rhs_s")})
+        self.red = torch.zeros(16, dtype=f64)
+        self.device = torch.device("cpu")
+        self.msum = None
+
+    def create(self, msum, hist_cap):
+        self.msum = msum
+
+    def sync(self):
+        pass
+
+    def gather(self, idx, src, dst):
+        s = self.v[src] if isinstance(src, str) else src
+        dst[: idx.numel()] = s.index_select(0, idx)
+
+    def begin(self, tol, max_iter, x0):
+        self.tol, self.max_iter = tol, max_iter
+        self.sc = {"rho": 0.0, "alpha": 0.0, "nb": 0.0, "mu1": 0.0, "mu2": 0.0, "beta": 0.0,
+                   "meanw": 0.0, "curv": float("nan")}
+        self.fl = {"done": False, "iters": 0, "conv": False, "bad": False, "zero": False,
+                   "maxit": False}
+        self.res, self.pre = [], []
+        self.v["x"].copy_(x0 if x0 is not None else self.v["x"] * 0.0)
+
+    def _split(self, a, x, nsplit, ghost):
+        import torch
+        return torch.as_tensor(a @ np.concatenate([x[:nsplit].numpy(), ghost.numpy()]))
+
+    def lambda_(self, which, ug, vg, use_flags):
+        if use_flags and self.fl["done"]:
+            return
+        n, m = self.n, self.m
+        v = self.v[which]
+        q = self.v["q"]
+        q[:n] = self._split(self.S1, v, n, ug[: self.lp.ghosts.size])
+        iv = self._split(self.Si, v[n:], m, vg[: self.lp.m_ghost])
+        q[:m] += iv
+        q[n:] = self._split(self.Si, v, m, ug[: self.lp.m_ghost]) + iv
+        q[n:] += self.lp.gamma * (_torch().as_tensor(self.lp.heart_mass) * v[n:])
+        self.red[0] = float((v * q).sum())
+
+    def init(self, b, has_x0):
+        n = self.n
+        r = self.v["r"]
+        r.copy_(b - self.v["q"] if has_x0 else b)
+        self.v["rhs_s"].copy_(r[n:])
+        self.red[1], self.red[2], self.red[3] = float((r * r).sum()), float(r[:n].sum()), float(
+            (b * b).sum())
+
+    def check(self, initial):
+        if self.fl["done"]:
+            return
+        if initial:
+            self.red[7] = self.red[3]
+            self.sc["nb"] = float(self.red[7]) ** 0.5
+            if self.sc["nb"] == 0.0:
+                self.fl.update(zero=True, conv=True, done=True)
+                self.res.append(0.0)
+                return
+        rel = float(self.red[1]) ** 0.5 / self.sc["nb"]
+        self.res.append(rel)
+        if not np.isfinite(rel):
+            self.fl.update(bad=True, done=True)
+        elif rel <= self.tol:
+            self.fl.update(conv=True, done=True)
+        elif not initial and self.fl["iters"] >= self.max_iter:
+            self.fl.update(maxit=True, done=True)
+        else:
+            self.sc["mu1"] = float(self.red[2]) / self.lp.n_global
+
+    def update(self):
+        if self.fl["done"]:
+            return
+        dq = float(self.red[0])
+        if not (np.isfinite(dq) and dq > 0.0):
+            self.fl.update(bad=True, done=True)
+            self.sc["curv"] = dq
+            return
+        a = self.sc["rho"] / dq
+        self.fl["iters"] += 1
+        x, r, d, q = (self.v[k] for k in ("x", "r", "d", "q"))
+        x += a * d
+        r -= a * q
+        self.v["rhs_s"].copy_(r[self.n:])
+        self.red[1], self.red[2] = float((r * r).sum()), float(r[: self.n].sum())
+
+    def pinv1(self):
+        if self.fl["done"]:
+            return
+        y = (self.v["r"][: self.n] - self.sc["mu1"]).numpy()
+        self.v["z1"].copy_(_torch().as_tensor(self.bulk.apply(y)))
+
+    def pinv2(self, tg):
+        if self.fl["done"] or self.m == 0:
+            return
+        rhs = self.v["rhs_s"] - self._split(self.Si, self.v["z1"], self.m, tg[: self.lp.m_ghost])
+        self.v["s"].copy_(_torch().as_tensor(self.schur.apply(rhs.numpy())))
+
+    def pinv3(self, sg):
+        if self.fl["done"]:
+            return
+        c = self.v["corr"]
+        if self.m:
+            c[: self.m] = self._split(self.Si, self.v["s"], self.m, sg[: self.lp.m_ghost])
+        self.red[3] = float(c[: self.m].sum())
+
+    def pinv4(self):
+        if self.fl["done"]:
+            return
+        self.sc["mu2"] = float(self.red[3]) / self.lp.n_global
+        y = (self.v["corr"] - self.sc["mu2"]).numpy()
+        z2 = _torch().as_tensor(self.bulk.apply(y))
+        w = self.v["z1"] - z2
+        self.v["z1"].copy_(w)
+        n = self.n
+        self.red[4], self.red[5] = float(w.sum()), float((self.v["r"][:n] * w).sum())
+        self.red[6] = float((self.v["r"][n:] * self.v["s"]).sum())
+
+    def finish(self, initial):
+        if self.fl["done"]:
+            return
+        mw = float(self.red[4]) / self.lp.n_global
+        rho = float(self.red[5]) - mw * float(self.red[2]) + float(self.red[6])
+        self.pre.append(rho)
+        beta = 0.0 if initial else rho / self.sc["rho"]
+        self.sc.update(meanw=mw, rho=rho, beta=beta)
+        d = self.v["d"]
+        if initial:
+            d.zero_()
+        d[: self.n] = (self.v["z1"] - mw) + beta * d[: self.n]
+        d[self.n:] = self.v["s"] + beta * d[self.n:]
+
+    def tg_buffer(self, plan):
+        return plan.tg
+
+    def wmean(self):
+        self.red[8] = float((_torch().as_tensor(self.lp.mass) * self.v["x"][: self.n]).sum())
+
+    def normalize(self, out):
+        if self.fl["zero"]:
+            out.zero_()
+            return
+        out.copy_(self.v["x"])
+        out[: self.n] -= float(self.red[8]) / self.msum
+
+    def done(self):
+        return self.fl["done"]
+
+    def read(self, cap):
+        f = self.fl
+        return {"iterations": f["iters"], "converged": f["conv"], "breakdown": f["bad"],
+                "zero_rhs": f["zero"], "max_iter": f["maxit"], "residual_history": list(self.res),
+                "preconditioned_history": list(self.pre), "curvature": self.sc["curv"]}
+
+
+class ShardSolver:
+    """The sharded deflated PCG (bd/krylov.py:46-140, block-Jacobi block-LU
+    preconditioner bd/precond.py:281-312) of one rank: halo exchanges and the
+    four all-reduces per iteration around the rank-local kernels of `ops`
+    (NativeShard on the box, TorchShard in the CPU tests).  On a CUDA device
+    one iteration, collectives included, is captured into a CUDA graph and
+    replayed; the host reads the done flag every `check_every` iterations
+    (replays past the end are device no-ops)."""
+
+    def __init__(self, lp: "LocalProblem", comm: Comm, ops):
+        self.lp, self.comm, self.ops = lp, comm, ops
+        self.plan = HaloPlan(lp, ops.device, ops.gather)
+        self.msum = comm.allreduce([float(np.sum(lp.mass))])[0]
+        self.graph = None
+        self._graph_key = None
+        self.graph_error = None
+        self.body_launches = 0      # native kernels in one captured iteration
+        self.replayed_launches = 0  # launched by graph replays (not seen by ctx.launches)
+
+    def _pinv(self, initial):
+        ops, plan, comm = self.ops, self.plan, self.comm
+        ops.pinv1()
+        tg = ops.tg_buffer(plan)
+        plan.halo_h(comm, ops.ptr["z1"] if hasattr(ops, "ptr") else "z1", tg)
+        ops.pinv2(tg)
+        plan.halo_h(comm, ops.ptr["s"] if hasattr(ops, "ptr") else "s", plan.sg)
+        ops.pinv3(plan.sg)
+        comm.allreduce_(ops.red[3:4])
+        ops.pinv4()
+        comm.allreduce_(ops.red[4:7])
+        ops.finish(initial)
+
+    def _body(self):
+        ops, plan, comm = self.ops, self.plan, self.comm
+        plan.halo_d(comm, ops.ptr["d"] if hasattr(ops, "ptr") else "d")
+        ops.lambda_("d", plan.ug, plan.vg, 1)
+        comm.allreduce_(ops.red[0:1])
+        ops.update()
+        comm.allreduce_(ops.red[1:3])
+        ops.check(0)
+        self._pinv(0)
+
+    def solve(self, b, x0=None, tol=1e-6, max_iter=500, check_every=16, graph=None):
+        """b, x0: this rank's [u_own | v_own] (device tensors).  Returns
+        (normalised x, stats dict); raises NonConvergenceError /
+        NumericalBreakdownError with the stats (bd/krylov.py:103-108, 133-139)."""
+        torch = _torch()
+        if tol <= 0:
+            raise ValueError("tol must be strictly positive")
+        ops, plan, comm = self.ops, self.plan, self.comm
+        h_before = getattr(ops, "h", None)
+        ops.create(self.msum, max(max_iter + 2, 20002))
+        if getattr(ops, "h", None) is not h_before:
+            self.graph, self._graph_key = None, None  # new device buffers: recapture
+        ops.sync()
+        ops.begin(tol, max_iter, x0)
+        if x0 is not None:
+            plan.halo_d(comm, ops.ptr["x"] if hasattr(ops, "ptr") else "x")
+            ops.lambda_("x", plan.ug, plan.vg, 0)
+        ops.init(b, x0 is not None)
+        comm.allreduce_(ops.red[1:4])
+        ops.check(1)
+        self._pinv(1)
+        dev = b.device
+        use_graph = (graph if graph is not None else
+                     (dev.type == "cuda" and getattr(comm, "capturable", True)
+                      and os.environ.get("BD_SHARDED_GRAPH", "1") != "0"))
+        k = 0
+        if not ops.done():
+            if use_graph and self.graph is None and self._graph_key != id(ops):
+                self._graph_key = id(ops)
+                self._capture()
+            g = self.graph if use_graph else None
+            while k < max_iter:
+                if g is not None:
+                    g.replay()
+                    self.replayed_launches += self.body_launches
+                else:
+                    self._body()
+                k += 1
+                if (k % check_every == 0 or k == max_iter) and ops.done():
+                    break
+            if not ops.done() and k >= max_iter:
+                pass  # the device already flagged max_iter on the last check
+        ops.wmean()
+        comm.allreduce_(ops.red[8:9])
+        out = torch.empty_like(b)
+        ops.normalize(out)
+        st = ops.read(max_iter + 2)
+        st["graph"] = self.graph is not None and use_graph
+        if self.graph_error:
+            st["graph_error"] = self.graph_error
+        st["mv_count"] = st["iterations"] + 1 + (1 if st["breakdown"] else 0)
+        from .errors import NonConvergenceError, NumericalBreakdownError
+        from .krylov import SolveStats
+        stats = SolveStats(iterations=st["iterations"], residual_history=st["residual_history"],
+                           preconditioned_history=st["preconditioned_history"],
+                           mv_count=st["mv_count"], p1_count=2 * st["iterations"],
+                           pk_count=st["iterations"], converged=st["converged"])
+        if st["breakdown"]:
+            raise NumericalBreakdownError(
+                f"conjugate gradient breakdown: curvature {st['curvature']}", stats=stats)
+        if not st["converged"]:
+            raise NonConvergenceError(f"PCG did not reach tol={tol} within {max_iter} iterations",
+                                      stats=stats)
+        return out, st
+
+    def _capture(self):
+        """One iteration (kernels, halos, all-reduces) into a CUDA graph."""
+        torch = _torch()
+        dev = self.ops.device
+        from . import _lib
+        ctx = self.ops.ctx
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        try:
+            g = torch.cuda.CUDAGraph()
+            l0 = ctx.launches()
+            with torch.cuda.graph(g, stream=side):
+                ctx.sync_stream()
+                self._body()
+            self.body_launches = ctx.launches() - l0
+            self.graph = g
+        except Exception as e:  # capture unsupported here (e.g. P2P in capture): eager body
+            self.graph = None
+            self.graph_error = f"{type(e).__name__}: {e}"[:300]
+        torch.cuda.current_stream(dev).wait_stream(side)
+        ctx.sync_stream()
+        _ = _lib
+
+
+def _cpu_inner(kind):
+    """Oracle inner solves for TorchShard (CPU tests only)."""
+    def make(a):
+        from oracle import bidomain_oracle as orc
+        return orc.make_inner(kind, a)
+    return make
 
 
 # ---- per-rank setup without global matrices (large meshes) --------------------------
@@ -538,8 +795,8 @@ def _rows_mass(mesh, space, owned_rows):
 
 def ghost_sets(mesh, part: np.ndarray, nprocs: int):
     """Ghost vertices of every rank from the element connectivity: vertices
-    of other ranks sharing an element with an owned vertex (heart first,
-    then torso, each ascending — the order build_local uses)."""
+    of other ranks sharing an element with an owned vertex, in the order
+    build_local uses (order_ghosts: heart then torso, grouped by owner)."""
     el = mesh.elements
     m = mesh.heart_vertex_count
     pe = part[el]
@@ -547,8 +804,7 @@ def ghost_sets(mesh, part: np.ndarray, nprocs: int):
     for r in range(nprocs):
         touch = (pe == r).any(axis=1)
         v = np.unique(el[touch])
-        g = v[part[v] != r]
-        out.append(np.concatenate([g[g < m], g[g >= m]]))
+        out.append(order_ghosts(v[part[v] != r], m, part))
     return out
 
 
@@ -661,29 +917,29 @@ def build_local_from_mesh(mesh, params, fibers, dt, part: np.ndarray, rank: int,
 
 class DistributedSimulation:
     """Sharded time loop: membrane RHS and gate on the owned heart vertices
-    (sm_100a kernels), the coupled solve by distributed_pcg."""
+    (sm_100a kernels), the coupled solve by ShardSolver over NativeShard."""
 
-    def __init__(self, wl, part: np.ndarray, rank: int, nprocs: int, dist, device, inner=None):
+    def __init__(self, wl, part: np.ndarray, rank: int, nprocs: int, dist, device, inner=None,
+                 comm=None):
         import torch
 
         from . import _lib
         from .ionic import site_masks
 
         self.wl = wl
-        self.comm = Comm(dist, device)
+        self.comm = comm or Comm(dist, device)
         self.lp = build_local_from_mesh(wl.mesh, wl.params, wl.fibers, wl.dt, part, rank, nprocs,
                                         comm_allreduce=self.comm.allreduce,
                                         assembly=os.environ.get("BD_ASSEMBLY", "device"))
-        self.backend = NativeBackend()
-        self.dsys = DistributedSystem(self.lp, self.comm, self.backend)
-        self.prec = DistributedBlockLU(self.dsys, inner or wl.inner, self.lp.beta)
+        self.ctx = _lib.Context.default()
+        self.shard = NativeShard(self.lp, inner or wl.inner, self.ctx)
+        self.solver = ShardSolver(self.lp, self.comm, self.shard)
         lp = self.lp
         pts = wl.mesh.vertices[lp.owned[: lp.m_own]]
         masks = site_masks(pts, wl.protocol) if wl.protocol.sites else None
         self.mask = (torch.as_tensor(masks.view(np.int64)).to(device) if masks is not None
                      else None)
         self.mh = torch.as_tensor(lp.heart_mass, device=device)
-        self.ctx = _lib.Context.default()
         self._lib = _lib
         self.device = device
 
@@ -701,14 +957,14 @@ class DistributedSimulation:
         u, v, w, t = state
         lp, wl, L = self.lp, self.wl, self._lib
         ion = wl.ionic
+        self.ctx.sync_stream()
         rhs = torch.empty(lp.n_own + lp.m_own, dtype=torch.float64, device=self.device)
         L.check(L.lib().bd_membrane_rhs_raw(
             self.ctx.handle, lp.n_own, lp.m_own, L.ptr(self.mh), lp.gamma, L.ptr(v), L.ptr(w),
             L.ptr(self.mask), int(active_sites(t, wl.protocol)), float(wl.protocol.amplitude),
             float(wl.params.chi), float(ion.v_rest), float(ion.v_span), float(ion.tau_in),
             float(ion.tau_out), float(wl.params.c_m), L.ptr(rhs), None), self.ctx.handle)
-        x, st = distributed_pcg(self.dsys, self.prec, rhs, tol=wl.tol, max_iter=20000,
-                                x0=torch.cat([u, v]))
+        x, st = self.solver.solve(rhs, x0=torch.cat([u, v]), tol=wl.tol, max_iter=20000)
         v_new = x[lp.n_own:].contiguous()
         w_new = torch.empty_like(w)
         L.check(L.lib().bd_membrane_gate(

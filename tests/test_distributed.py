@@ -1,38 +1,19 @@
 """CPU (gloo, world size 2): the sharded path's host logic — RCB partition,
-heart-first local numbering, one-layer halo plan, distributed Λ and the
-distributed block-Jacobi PCG — against the single-process oracle on the
-golden config-2 slab.  Local compute uses a scipy test double for the
-backend (the product backend is paper_1711_08708_b200.distributed.NativeBackend)."""
+heart-first local numbering with ghosts grouped by owner, the halo plan, the
+four all-reduces per iteration and the block-Jacobi PCG loop of
+ShardSolver — against the single-process oracle on the golden config-2
+slab.  The rank-local kernels run in TorchShard, the CPU restatement of the
+native bd_shard_* kernels (the product path is NativeShard; its GPU tests are
+tests/test_gpu_distributed.py)."""
 import os
 import socket
 
 import numpy as np
 import pytest
-import scipy.sparse as sp
-import scipy.sparse.linalg as spla
 
 from conftest import REPO, csr, golden
 
 from paper_1711_08708_b200 import distributed as D
-
-
-class ScipyBackend:
-    """Test double: local SpMV and block inner solves with scipy on CPU tensors."""
-
-    def matrix(self, a):
-        return sp.csr_matrix(a)
-
-    def spmv(self, a, x):
-        import torch
-        return torch.as_tensor(a @ x.numpy())
-
-    def inner(self, kind, a, coords=None):
-        from oracle import bidomain_oracle as orc
-        return orc.make_inner(kind, a)
-
-    def inner_apply(self, p, y):
-        import torch
-        return torch.as_tensor(p.apply(y.numpy()))
 
 
 def test_rcb_partition_balanced_boxes():
@@ -87,11 +68,13 @@ def _worker(rank, world, port, inner, out_dir):
         part = D.rcb_partition(g["points"], world)
         lp = D.build_local(S1, Si, g["mass"], g["mh"], g["gamma"], grounded, Km, part, rank, world)
         comm = D.Comm(dist, torch.device("cpu"))
-        dsys = D.DistributedSystem(lp, comm, ScipyBackend())
-        pre = D.DistributedBlockLU(dsys, inner, beta)
+        solver = D.ShardSolver(lp, comm, D.TorchShard(lp, D._cpu_inner(inner)))
         bu, bv = g["sanity_b_u"], g["sanity_b_v"]
         b = torch.as_tensor(np.concatenate([bu[lp.owned], bv[lp.owned[: lp.m_own]]]))
-        x, st = D.distributed_pcg(dsys, pre, b, tol=1e-10, max_iter=5000)
+        x, st = solver.solve(b, tol=1e-10, max_iter=5000)
+        # the four all-reduces of an iteration leave the residual history of
+        # the recursive residual on every rank identical
+        assert len(st["residual_history"]) == st["iterations"] + 1
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=x.numpy(), owned=lp.owned,
                  m_own=lp.m_own, iters=st["iterations"])
     finally:
@@ -132,6 +115,68 @@ def test_distributed_pcg_gloo_world2(inner, tmp_path):
         assert iters[0] <= 3 * int(g["sanity_ic0_iters"])
 
 
+def _torso_problem():
+    """Heart-in-torso 2D mesh (heart-first numbering, torso AND heart ghosts)."""
+    from oracle import bidomain_oracle as orc
+    from paper_1711_08708_b200 import configs
+    from paper_1711_08708_b200.precond import build_monodomain_matrix
+    from paper_1711_08708_b200.system import BidomainSystem
+    wl = configs.cfg1(40)
+    sysm = BidomainSystem.build(wl.mesh, wl.params, wl.dt, fibers=wl.fibers, with_extra=False)
+    km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
+    beta, grounded = orc.regularize(sysm.stiff_total)
+    bu, bv = configs.sanity_rhs(sysm.n, sysm.n_heart, seed=3)
+    return wl, sysm, km, grounded, bu, bv
+
+
+def _torso_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl, sysm, km, grounded, bu, bv = _torso_problem()
+        part = D.rcb_partition(wl.mesh.vertices, world)
+        lp = D.build_local(sysm.stiff_total, sysm.stiff_intra, sysm.mass_diag,
+                           sysm.heart_mass_diag, sysm.gamma, grounded, km, part, rank, world)
+        assert lp.m_ghost < lp.ghosts.size  # torso ghosts present
+        solver = D.ShardSolver(lp, D.Comm(dist, torch.device("cpu")),
+                               D.TorchShard(lp, D._cpu_inner("jacobi")))
+        b = torch.as_tensor(np.concatenate([bu[lp.owned], bv[lp.owned[: lp.m_own]]]))
+        x, st = solver.solve(b, tol=1e-10, max_iter=20000)
+        np.savez(os.path.join(out_dir, f"t{rank}.npz"), x=x.numpy(), owned=lp.owned,
+                 m_own=lp.m_own, iters=st["iterations"])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_pcg_gloo_world2_heart_in_torso(tmp_path):
+    """World size 2 on a heart-in-torso mesh: the S_i products read only the
+    heart ghosts, Λ the heart and torso ghosts; jacobi shards exactly, so the
+    sharded solve equals the oracle's (iterations +-2, rel-L2 1e-8)."""
+    import torch.multiprocessing as mp
+    from oracle import bidomain_oracle as orc
+    world = 2
+    mp.spawn(_torso_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    wl, sysm, km, grounded, bu, bv = _torso_problem()
+    pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, "jacobi")
+    (ru, rv), st = orc.pcg(sysm.stiff_total, sysm.stiff_intra, sysm.heart_mass_diag,
+                           sysm.mass_diag, sysm.gamma, pre, bu, bv, tol=1e-10, max_iter=20000)
+    xu, xv = np.zeros(sysm.n), np.zeros(sysm.n_heart)
+    iters = []
+    for r in range(world):
+        d = np.load(tmp_path / f"t{r}.npz")
+        own, mo = d["owned"], int(d["m_own"])
+        xu[own] = d["x"][: own.size]
+        xv[own[:mo]] = d["x"][own.size:]
+        iters.append(int(d["iters"]))
+    assert iters[0] == iters[1] and abs(iters[0] - st["iterations"]) <= 2
+    rel = np.sqrt(np.sum((xu - ru) ** 2) + np.sum((xv - rv) ** 2)) / np.sqrt(
+        np.sum(ru ** 2) + np.sum(rv ** 2))
+    assert rel <= 1e-8
+
+
 def test_local_assembly_matches_global():
     """Per-rank assembly from the touching elements reproduces the rows of the
     global matrices and the global halo plan."""
@@ -164,18 +209,3 @@ def test_local_assembly_matches_global():
             assert np.array_equal(ref.recv[q], loc.recv[q])
         for q in ref.send_heart:
             assert np.array_equal(ref.send_heart[q], loc.send_heart[q])
-
-
-def test_weak_scaling_grids():
-    """bench.py --mode sharded refines the cfg2 slab so every rank keeps a
-    cfg2-sized part; 8 ranks is exactly BASELINE config 3 (256x256x128)."""
-    import importlib.util
-    spec = importlib.util.spec_from_file_location("bench", os.path.join(REPO, "bench.py"))
-    b = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(b)
-    base = (128, 128, 64)
-    assert b.weak_cells(base, 1) == base
-    assert b.weak_cells(base, 8) == (256, 256, 128)
-    for w in (1, 2, 4, 8, 16):
-        c = b.weak_cells(base, w)
-        assert c[0] * c[1] * c[2] == w * base[0] * base[1] * base[2]
