@@ -299,9 +299,21 @@ bd_status fail(bd_ctx* ctx, bd_status st, const std::string& msg) {
     if (st_ != BD_OK) return st_; \
   } while (0)
 
+// BD_POISON=1: every library allocation starts as all-ones bytes (a NaN
+// pattern), so a kernel that reads device memory nothing wrote turns the
+// results into NaN and the parity tests catch it (tests/test_gpu_poison.py;
+// the pool's compute-sanitizer is closed).
+static bool poison_allocs() {
+  static const bool on = getenv("BD_POISON") && atoi(getenv("BD_POISON")) != 0;
+  return on;
+}
+
 template <class T>
 cudaError_t dalloc(T** p, int64_t count) {
-  return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1));
+  const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+  cudaError_t e = cudaMalloc((void**)p, bytes);
+  if (e == cudaSuccess && poison_allocs()) e = cudaMemset(*p, 0xFF, bytes);
+  return e;
 }
 
 static double wall_s() {
