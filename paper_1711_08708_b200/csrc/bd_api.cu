@@ -256,6 +256,7 @@ struct bd_prec {
   Ctl ctl{};       // PCG control block (flags on)
   Ctl ctl_nf{};    // same storage, flags off (standalone applies, final normalise)
   double *traw, *z2raw, *corr, *sbuf;  // P^{-1} scratch
+  double* zsc = nullptr;               // zero scalar slots (PCG-internal RhsSchur)
   double *x, *r, *z, *d, *q;           // PCG vectors (n+m)
   int hist_cap = 0;
   // CUDA graph of one PCG iteration inside a WHILE node
@@ -1745,8 +1746,13 @@ bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
 // P_Λ^{-1} r (bd/precond.py:298-312) with sc[MU1], sc[C1] already holding
 // mean(r_u) and mean(r_u)/beta.  zu: output u-block; zv_int: polled Schur
 // output (sentinel-filled); zv_out: nullable scatter copy of it.
+// in_pcg (the PCG loop, whose next step deflates z_u, bd/krylov.py:41-43):
+// the two bulk solves skip their output means (constants on z_u that the
+// deflation removes; S_i t = S_i t_raw because S_i 𝟙 = 0), and the tail
+// forms z_u = t_raw − z2_raw together with the partials of rho (no k_rho).
+// The standalone apply keeps the reference's recentring (bd_blocklu_apply).
 bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, double* zv_out,
-                       const Ctl& c, bool deflate_sum) {
+                       const Ctl& c, bool in_pcg) {
   bd_system* s = p->sys;
   bd_ctx* ctx = s->ctx;
   const int64_t n = s->n, m = s->m;
@@ -1760,12 +1766,15 @@ bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, 
       xi = p->traw;
       out = nullptr;
     }
-    TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S, dev::FIN_MEAN, dev::S_MT, -1, n));
+    if (in_pcg)
+      TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S));
+    else
+      TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S, dev::FIN_MEAN, dev::S_MT, -1, n));
   }
   prof_mark(ctx, 2);
   // s = K^{-1}(r_v - S_i t[:m])
   {
-    dev::RhsSchur rhs{s->Si->dev(), p->traw, c.sc, r + n, p->schur->perm};
+    dev::RhsSchur rhs{s->Si->dev(), p->traw, in_pcg ? p->zsc : c.sc, r + n, p->schur->perm};
     double* xi = zv_int;
     double* out = zv_out;
     if (p->schur->perm) {
@@ -1791,11 +1800,19 @@ bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, 
       xi = p->z2raw;
       out = nullptr;
     }
-    TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK2_S, dev::FIN_MEAN, dev::S_M2, -1, n));
+    if (in_pcg)
+      TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK2_S));
+    else
+      TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK2_S, dev::FIN_MEAN, dev::S_M2, -1, n));
   }
   prof_mark(ctx, 2);
-  dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(
-      p->traw, p->z2raw, zu, n, c, deflate_sum ? 1 : 0);
+  if (in_pcg) {
+    dev::k_combine_rho<<<grid_for(ctx, n + m, dev::TPB), dev::TPB, 0, ctx->stream>>>(
+        p->traw, p->z2raw, zu, zv_out ? zv_out : zv_int, r, n, n + m, c);
+  } else {
+    dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->traw, p->z2raw, zu, n,
+                                                                          c, 0);
+  }
   LAUNCHED(ctx);
   prof_mark(ctx, 5);
   return BD_OK;
@@ -1813,9 +1830,7 @@ bd_status enqueue_iteration(bd_prec* p) {
                                                                            nm, c);
   LAUNCHED(ctx);
   prof_mark(ctx, 1);
-  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));
-  dev::k_rho<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->r, p->z, n, nm, c);
-  LAUNCHED(ctx);
+  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));  // rho in its tail
   dev::k_dupdate<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->z, p->d, n, nm, c);
   LAUNCHED(ctx);
   prof_mark(ctx, 5);
@@ -2504,7 +2519,8 @@ bd_status bd_blocklu_create(bd_system* s, bd_inner* bulk, bd_inner* schur, doubl
   p->hist_cap = 0;
   if (ctl_alloc(&p->ctl, parts, 0, 1) || dalloc(&p->traw, n) || dalloc(&p->z2raw, n) ||
       dalloc(&p->corr, m) || dalloc(&p->sbuf, m) || dalloc(&p->x, nm) || dalloc(&p->r, nm) ||
-      dalloc(&p->z, nm) || dalloc(&p->d, nm) || dalloc(&p->q, nm)) {
+      dalloc(&p->z, nm) || dalloc(&p->d, nm) || dalloc(&p->q, nm) || dalloc(&p->zsc, dev::NSLOTS) ||
+      cudaMemset(p->zsc, 0, sizeof(double) * dev::NSLOTS)) {
     bd_blocklu_destroy(p);
     return fail(ctx, BD_ECUDA, "bd_blocklu_create: allocation failed");
   }
@@ -2529,6 +2545,7 @@ bd_status bd_blocklu_destroy(bd_prec* p) {
   if (p->graph) cudaGraphDestroy(p->graph);
   ctl_free(&p->ctl);
   cudaFree(p->traw);
+  cudaFree(p->zsc);
   cudaFree(p->z2raw);
   cudaFree(p->corr);
   cudaFree(p->sbuf);
@@ -2683,9 +2700,7 @@ bd_status bd_pcg_solve(bd_system* s, bd_prec* p, const double* b, const double* 
   LAUNCHED(ctx);
   prof_mark(ctx, 1);
   // z0 = deflate(P^{-1} r0); rho0; d0 = z0
-  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));
-  dev::k_rho<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->r, p->z, n, nm, c);
-  LAUNCHED(ctx);
+  TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));  // rho in its tail
   dev::k_dupdate<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->z, p->d, n, nm, c);
   LAUNCHED(ctx);
   prof_mark(ctx, 5);

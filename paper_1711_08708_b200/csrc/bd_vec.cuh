@@ -193,6 +193,36 @@ __global__ void __launch_bounds__(TPB) k_combine(const double* __restrict__ traw
   }
 }
 
+// PCG-internal P^{-1} tail: z_u = t_raw − z2_raw (the recentrings of the two
+// bulk solves are constants and fall out under the deflation), and the
+// partials of Σz_u, r_u·z_u, r_v·z_v for rho (FIN_RHO3) in the same pass
+__global__ void __launch_bounds__(TPB) k_combine_rho(const double* __restrict__ traw,
+                                                     const double* __restrict__ z2raw,
+                                                     double* __restrict__ zu,
+                                                     const double* __restrict__ zv,
+                                                     const double* __restrict__ r, int64_t n,
+                                                     int64_t nm, Ctl c) {
+  if (inactive(c)) return;
+  __shared__ double sm[32];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      const double z = __dsub_rn(traw[i], z2raw[i]);
+      zu[i] = z;
+      a0 += z;
+      a1 = fma(r[i], z, a1);
+    } else {
+      a2 = fma(r[i], zv[i - n], a2);
+    }
+  }
+  double v[3];
+  v[0] = block_sum(a0, sm);
+  v[1] = block_sum(a1, sm);
+  v[2] = block_sum(a2, sm);
+  reduce_tail<3>(c, v, gridDim.x, blockIdx.x, C_RHO, FIN_RHO3, 0, -1, n, sm);
+}
+
 // rho = r·z with z_u deflated on the fly (`_deflate`, bd/krylov.py:41-43;
 // `r.dot(z)`, :96 / :126)
 __global__ void __launch_bounds__(TPB) k_rho(const double* __restrict__ r, const double* __restrict__ z,
