@@ -316,7 +316,7 @@ def run_native(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world == 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic structured mesh, seeded/defined stimulus; "
                     "no dataset)",
             "config": {"workload": f"{wl.name}: {wl.description}", "dof": n + m, "n": n,
@@ -599,7 +599,7 @@ def run_reference(args, rank):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6) if value else None,
             "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * total / args.steps, 1), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic structured mesh)",
             "config": {"workload": f"{wl.name}: {wl.description}", "dof": n + m,
                        "inner": wl.inner, "tol": wl.tol,
