@@ -194,6 +194,7 @@ struct bd_inner {
   int64_t n;
   int G = 8;
   int prof_cls = 2;  // profile class of its triangular passes (2 bulk, 3 Schur)
+  int fold_fill = 0; // BD_FOLD_FILL (see inner_solve_g)
   DevTri L, U;
   bool super = false;
   DevSuper SL, SU;
@@ -1359,14 +1360,15 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
 
 template <class Rhs>
 bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
-                       int ctr_task, int ctr_done, double* reset) {
+                       int ctr_task, int ctr_done, double* reset, double* r0 = nullptr,
+                       double* r1 = nullptr) {
   bd_ctx* ctx = p->ctx;
   if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr);
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else if (b.reg && !reset)
     dev::k_trsv_rtile<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr);
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else
     dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
                                                                        ctr_done, reset);
@@ -1493,22 +1495,31 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
           (int)p->n, rhs, p->rhs_pre, c);
       LAUNCHED(ctx);
     }
-    dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
-                                                                  dev::SENTINEL, c);
-    LAUNCHED(ctx);
+    // BD_FOLD_FILL: 1 = the forward pass resets the backward's output rows
+    // (no fill before the backward); 2 = also the backward pass resets the
+    // forward output it gathers (y_int stays sentinel between solves)
+    const int fold = (ib || !p->BL.reg || !p->BU.reg || p->rhs_pre) ? 0 : p->fold_fill;
+    if (fold < 2) {
+      dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
+                                                                    dev::SENTINEL, c);
+      LAUNCHED(ctx);
+    }
     prof_mark(ctx, 5);  // (profile classes: fills and dots are vector work,
                         //  the two passes alone are the triangular-solve class)
     if (!Rhs::kScalar && p->rhs_pre)
       TRY(launch_btile(p, p->BL, dev::RhsVec{p->rhs_pre, (int)p->n, nullptr, nullptr}, p->y_int, c,
                        ctr0, ctr0 + 1, nullptr));
     else
-      TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr));
+      TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr, fold ? xg : nullptr));
     prof_mark(ctx, p->prof_cls);
-    dev::k_fill<<<grid_for(ctx, nf2, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : xg, nf2,
-                                                                  dev::SENTINEL, c);
-    LAUNCHED(ctx);
+    if (fold < 1) {
+      dev::k_fill<<<grid_for(ctx, nf2, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : xg, nf2,
+                                                                    dev::SENTINEL, c);
+      LAUNCHED(ctx);
+    }
     prof_mark(ctx, 5);
-    TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr));
+    TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr, nullptr,
+                     fold >= 2 ? p->y_int : nullptr));
     prof_mark(ctx, p->prof_cls);
     if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     prof_mark(ctx, 5);
@@ -2381,6 +2392,11 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
     bd_inner_destroy(p);
     return fail(ctx, BD_ECUDA, "bd_inner_create: allocation failed");
   }
+  // default 1: the forward pass resets the backward pass's output rows
+  // (measured cfg2 1.433 -> 1.412 ms per PCG iteration); 2 also folds the
+  // forward output's reset into the previous backward pass, which loses its
+  // L2 residency and measured 1.82 ms per iteration
+  p->fold_fill = getenv("BD_FOLD_FILL") ? atoi(getenv("BD_FOLD_FILL")) : 1;
   if (!p->hperm.empty()) {
     if (dalloc(&p->perm, n) ||
         cudaMemcpy(p->perm, p->hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice)) {

@@ -1155,7 +1155,8 @@ template <bool kSmemInv, bool kTileRhs, class Rhs>
 __global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
     k_trsv_rtile(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
                  const double* __restrict__ bt, const int* __restrict__ opos,
-                 double* __restrict__ bt_next) {
+                 double* __restrict__ bt_next, double* reset0 = nullptr,
+                 double* reset1 = nullptr) {
   if (inactive(c)) return;
   extern __shared__ __align__(16) double rt_sm[];
   double* ys = rt_sm;                 // RT_ROWS
@@ -1252,6 +1253,13 @@ __global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
       b = rhs.template eval<1>(row, 0);
     } else {
       b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
+    }
+    // sentinel resets folded into the pass (BD_FOLD_FILL): reset0 = the next
+    // pass's polled output, reset1 = this pass's gathered right-hand side
+    // (the forward output, read above) for the inner's next forward pass
+    if (g == 0 && row >= 0) {
+      if (reset0) reset0[row] = __longlong_as_double(SENTINEL);
+      if (reset1) reset1[row] = __longlong_as_double(SENTINEL);
     }
     if (trace) {
       __syncthreads();
