@@ -222,13 +222,56 @@ class DeviceAssembler:
         return out
 
     def _run(self, el, nv, sigma, sigma2=None, space=Space.FULL):
+        """Assemble on the device.  Meshes whose (element, local pair) keys
+        exceed BD_ASSEMBLY_MAX_PAIRS (default 6e8, ~25 GB of device scratch)
+        are assembled in row blocks: each block's rows from the elements that
+        touch them (a local mesh), the same per-entry element order as one
+        pass, so the result is identical."""
+        arity = self.mesh.dim + 1
+        max_pairs = float(os.environ.get("BD_ASSEMBLY_MAX_PAIRS", "6e8"))
+        if el.shape[0] * arity * arity > max_pairs:
+            return self._run_blocks(el, nv, sigma, sigma2, space, max_pairs)
+        return self._run_one(self.verts, el, nv, sigma, sigma2, space)
+
+    def _run_blocks(self, el, nv, sigma, sigma2, space, max_pairs):
+        arity = self.mesh.dim + 1
+        nblk = int(np.ceil(2.0 * el.shape[0] * arity * arity / max_pairs))
+        bounds = np.linspace(0, nv, nblk + 1).astype(np.int64)
+        ips, ixs, dvs, masses = [np.zeros(1, dtype=np.int64)], [], [], []
+        off = 0
+        for r0, r1 in zip(bounds[:-1], bounds[1:]):
+            if r1 <= r0:
+                continue
+            touch = ((el >= r0) & (el < r1)).any(axis=1)
+            sub = el[touch]
+            lv = np.unique(sub)
+            loc = np.ascontiguousarray(np.searchsorted(lv, sub), dtype=np.int64)
+            s1 = np.ascontiguousarray(sigma[touch])
+            s2 = None if sigma2 is None else np.ascontiguousarray(sigma2[touch])
+            a, mass = self._run_one(np.ascontiguousarray(self.verts[lv]), loc, lv.size, s1, s2,
+                                    None)
+            i0, i1 = np.searchsorted(lv, r0), np.searchsorted(lv, r1)
+            rows = a[i0:i1]
+            ips.append(rows.indptr[1:].astype(np.int64) + off)
+            off += rows.nnz
+            ixs.append(lv[rows.indices].astype(np.int32))
+            dvs.append(rows.data)
+            masses.append(mass[i0:i1])
+            del a, rows, touch, sub, loc, s1, s2
+        mat = sp.csr_matrix((np.concatenate(dvs), np.concatenate(ixs), np.concatenate(ips)),
+                            shape=(nv, nv))
+        mass = np.concatenate(masses)
+        self._mass.setdefault(space, mass)
+        return mat, mass
+
+    def _run_one(self, verts, el, nv, sigma, sigma2=None, space=Space.FULL):
         L = self._lib
         C = __import__("ctypes")
         h = C.c_void_p()
         nnz = C.c_int64()
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
         s2 = None if sigma2 is None else np.ascontiguousarray(sigma2, dtype=np.float64)
-        st = L.lib().bd_assemble_p1(self.ctx.handle, self.mesh.dim, int(nv), self.verts.ctypes.data,
+        st = L.lib().bd_assemble_p1(self.ctx.handle, self.mesh.dim, int(nv), verts.ctypes.data,
                                     int(el.shape[0]), el.ctypes.data, sigma.ctypes.data,
                                     None if s2 is None else s2.ctypes.data, C.byref(h),
                                     C.byref(nnz))
@@ -246,7 +289,8 @@ class DeviceAssembler:
                     self.ctx.handle)
         finally:
             L.lib().bd_assemble_destroy(h)
-        self._mass.setdefault(space, mass)
+        if space is not None:
+            self._mass.setdefault(space, mass)
         return sp.csr_matrix((data, indices, indptr), shape=(nv, nv)), mass
 
     def stiffness(self, kind: str) -> sp.csr_matrix:

@@ -117,3 +117,23 @@ def test_transmural_tensors_on_device(ortho):
     hi, he = tf._heart_tensors(wl.mesh.vertices[da.el_h].mean(axis=1))
     for dev, host in ((da.intra, hi), (da.extra, he)):
         assert np.abs(dev - host).max() <= 1e-14 * np.abs(host).max()
+
+
+def test_row_blocked_assembly_identical(monkeypatch):
+    """Meshes too large for one device pass are assembled in row blocks
+    (BD_ASSEMBLY_MAX_PAIRS); each block sees every element touching its rows
+    in the global element order, so the result equals the one-pass assembly
+    bit for bit (values, pattern, masses)."""
+    wl = configs.cfg4(20)
+    one = DeviceAssembler(wl.mesh, wl.params, wl.fibers)
+    ref = {k: one.stiffness(k) for k in ("bar1", "intra", "mono")}
+    mref = {s: one.lumped_mass(s) for s in (Space.FULL, Space.HEART_ONLY)}
+    monkeypatch.setenv("BD_ASSEMBLY_MAX_PAIRS", "20000")
+    blk = DeviceAssembler(wl.mesh, wl.params, wl.fibers)
+    for k, a in ref.items():
+        b = blk.stiffness(k)
+        np.testing.assert_array_equal(a.indptr, b.indptr)
+        np.testing.assert_array_equal(a.indices, b.indices)
+        np.testing.assert_array_equal(a.data.view(np.int64), b.data.view(np.int64))
+    for s, m in mref.items():
+        np.testing.assert_array_equal(m.view(np.int64), blk.lumped_mass(s).view(np.int64))

@@ -5,8 +5,10 @@
 IC(0) inners, `steps` semi-implicit steps from rest (apex stimulus).  Prints
 one JSON record per size, then the trend: growth rates of iterations*n between
 sizes (bd/bench.py:30-36), the least-squares slope of log(iters*n) vs log n,
-and alpha of iters ~ log(n)^alpha.  384^3 (57M vertices) is the 8-GPU case and
-does not fit one GPU's setup; the sweep stops at the largest size given.
+and alpha of iters ~ log(n)^alpha.  Sizes above ~300^3 assemble in row blocks
+(assembly.DeviceAssembler, BD_ASSEMBLY_MAX_PAIRS) and need
+BD_ASSEMBLY_REFZEROS=snap (no host assembly of a 57M-vertex torso); a watchdog
+exits cleanly if host memory runs low.
 
   python tools/cfg4_sweep.py --cells 96,128,160,192 --steps 20
 """
@@ -56,14 +58,38 @@ def run(cells, steps):
            "ms_per_iter": float(np.sum(dev_ms) / max(1, np.sum(iters))),
            "setup_s": {"mesh": round(t_mesh, 1), "assembly": round(t_asm, 1),
                        "precond": round(t_pre, 1)},
-           "probe_v_final": state.v.cpu().numpy()[wl.probes].tolist()}
+           "probe_v_final": state.v.cpu().numpy()[wl.probes].tolist(),
+           "gpu_mem_used_gb": round((torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9,
+                                    1),
+           "host_peak_rss_gb": round(__import__("resource").getrusage(
+               __import__("resource").RUSAGE_SELF).ru_maxrss / 1e6, 1)}
     print(json.dumps(rec), flush=True)
     del pre, sysm, km, state
     torch.cuda.empty_cache()
     return rec
 
 
+def _memory_watchdog(min_free_gb=10.0):
+    """Exit cleanly before the host runs out of memory (a host OOM would take
+    the box down); reports the peak host RSS."""
+    import threading
+
+    import psutil
+
+    def watch():
+        while True:
+            if psutil.virtual_memory().available < min_free_gb * 1e9:
+                print(json.dumps({"aborted": "host memory below %.0f GB free" % min_free_gb,
+                                  "rss_gb": round(psutil.Process().memory_info().rss / 1e9, 1)}),
+                      flush=True)
+                os._exit(99)
+            time.sleep(0.5)
+
+    threading.Thread(target=watch, daemon=True).start()
+
+
 def main():
+    _memory_watchdog()
     ap = argparse.ArgumentParser()
     ap.add_argument("--cells", default="96,128,160,192")
     ap.add_argument("--steps", type=int, default=20)
