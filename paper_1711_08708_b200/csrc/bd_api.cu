@@ -2294,6 +2294,8 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
       bd_inner_destroy(p);
       return fail(ctx, BD_EPRECOND, "sparse Cholesky failed, matrix not positive definite: " + msg);
     }
+    const double relax = getenv("BD_SUPER_RELAX") ? atof(getenv("BD_SUPER_RELAX")) : 0.0;
+    if (relax > 0.0) relax_supernodes(&lower, relax, dev::SN_MAX);
   }
   HostCsr upper = transpose(lower);
   const double avg = lower.n ? (double)lower.nnz() / lower.n : 1.0;

@@ -1049,4 +1049,54 @@ int partition_grid(int64_t n, int dim, const double* coords, int target,
   return (int)keys.size();
 }
 
+
+// Relaxed supernodes (exact inner): a row joins the current block of
+// consecutive rows [c0, i) when the dense triangle the supernodal solves
+// expect would miss at most frac·(i − c0) of the columns c0..i−1 in it; the
+// missing entries are inserted as explicit zeros, which change no result
+// (0·x adds nothing) but merge chains of small supernodes into fewer, larger
+// ones (fewer levels of the supernodal task DAG).  Blocks stop at smax rows.
+void relax_supernodes(HostCsr* L, double frac, int smax) {
+  const int64_t n = L->n;
+  if (n == 0 || !(frac > 0.0)) return;
+  HostCsr out;
+  out.n = n;
+  out.indptr.assign(n + 1, 0);
+  out.indices.reserve(L->indices.size() + L->indices.size() / 8);
+  out.values.reserve(L->values.size() + L->values.size() / 8);
+  int64_t c0 = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t b = L->indptr[i], e = L->indptr[i + 1];  // diagonal at e-1
+    const int64_t k = i - c0;
+    bool join = false;
+    if (i > 0 && k > 0 && k < smax) {
+      const int32_t* first = L->indices.data() + b;
+      const int32_t* last = L->indices.data() + (e - 1);
+      const int64_t present = last - std::lower_bound(first, last, (int32_t)c0);
+      const int64_t miss = k - present;
+      join = miss == 0 || (double)miss <= frac * (double)k;
+    }
+    if (!join) c0 = i;
+    int64_t q = b;
+    for (; q < e - 1 && L->indices[q] < c0; ++q) {  // external columns
+      out.indices.push_back(L->indices[q]);
+      out.values.push_back(L->values[q]);
+    }
+    for (int64_t j = c0; j < i; ++j) {  // the block's dense triangle row
+      if (q < e - 1 && L->indices[q] == j) {
+        out.indices.push_back((int32_t)j);
+        out.values.push_back(L->values[q]);
+        ++q;
+      } else {
+        out.indices.push_back((int32_t)j);
+        out.values.push_back(0.0);
+      }
+    }
+    out.indices.push_back((int32_t)i);  // diagonal last
+    out.values.push_back(L->values[e - 1]);
+    out.indptr[i + 1] = (int64_t)out.indices.size();
+  }
+  *L = std::move(out);
+}
+
 }  // namespace bd

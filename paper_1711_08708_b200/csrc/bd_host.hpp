@@ -47,6 +47,10 @@ void nested_dissection(const HostCsr& a, std::vector<int32_t>* perm);
 int cholesky(const HostCsr& a, const std::vector<int32_t>& perm, HostCsr* lower,
              std::string* msg);
 
+// Relaxed supernodes: explicit zeros completing near-dense triangles of
+// consecutive rows (see bd_host.cpp); frac = tolerated missing fraction.
+void relax_supernodes(HostCsr* L, double frac, int smax);
+
 }  // namespace bd
 
 namespace bd {
