@@ -2295,17 +2295,22 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
       return fail(ctx, BD_EPRECOND, "sparse Cholesky failed, matrix not positive definite: " + msg);
     }
     // relaxed supernodes (explicit zeros; measured on config 1's 263k-row bulk
-    // factor: frac 0 / 0.5 / 0.85 / 0.9 / 1.0 -> 15.1 / 14.2 / 13.7 / 13.7 /
-    // 1188 ms per time step, nnz(L) +18 % at 0.85)
-    const double relax = getenv("BD_SUPER_RELAX") ? atof(getenv("BD_SUPER_RELAX")) : 0.85;
-    if (relax > 0.0) relax_supernodes(&lower, relax, dev::SN_MAX);
+    // factor, profiles/r02_cfg1_relax_sweep.txt: none 15.1 ms per time step,
+    // frac 0.85 uncapped 13.7, frac 0.9 with blocks capped at 320 rows 12.5,
+    // frac 1.0 uncapped 1188; nnz(L) +18 %)
+    const double relax = getenv("BD_SUPER_RELAX") ? atof(getenv("BD_SUPER_RELAX")) : 0.9;
+    const int relax_max = getenv("BD_SUPER_RELAX_MAX") ? atoi(getenv("BD_SUPER_RELAX_MAX")) : 320;
+    if (relax > 0.0) relax_supernodes(&lower, relax, std::min(relax_max, dev::SN_MAX));
   }
   HostCsr upper = transpose(lower);
   const double avg = lower.n ? (double)lower.nnz() / lower.n : 1.0;
   p->G = pick_g(avg - 1.0);
   bd_status st = upload_tri(ctx, lower, true, p->G, &p->L);
   if (st == BD_OK) st = upload_tri(ctx, upper, false, p->G, &p->U);
-  const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 16384;
+  // dense explicit inverse up to 8192 rows (config 0: 0.62 vs 3.9 ms per
+  // step); above, the relaxed supernodal solves match it (config 1's 16k-row
+  // Schur block: 13.63 vs 13.71 ms per step) without the n^2 buffers
+  const int64_t dense_max = getenv("BD_EXACT_DENSE_MAX") ? atoll(getenv("BD_EXACT_DENSE_MAX")) : 8192;
   // the explicit inverse takes n^2 doubles on the host and on the device:
   // only when both have 4x that free (else the supernodal solves below)
   bool dense_fits = false;
