@@ -737,6 +737,37 @@ class ShardSolver:
         _ = _lib
 
 
+class HostStagedComm(Comm):
+    """Comm whose partial sums and halos travel through host memory over a
+    gloo process group.  For running several ranks on ONE GPU (tests and the
+    iteration-count study, tools/sharded_iters.py): no kernel ever waits on
+    another rank's kernels, the host does.  Not graph-capturable; not a
+    product path (NCCL over NVLink is)."""
+
+    capturable = False
+
+    def allreduce_(self, t):
+        if self.single:
+            return t
+        c = t.detach().cpu()
+        self.dist.all_reduce(c)
+        t.copy_(c)
+        return t
+
+    def exchange(self, sends, recvs):
+        torch = _torch()
+        if sends or recvs:
+            torch.cuda.synchronize()
+        ops = [self.dist.P2POp(self.dist.isend, buf.detach().cpu(), q) for q, buf in sends]
+        tmp = [(torch.empty(buf.numel(), dtype=buf.dtype), buf) for _, buf in recvs]
+        ops += [self.dist.P2POp(self.dist.irecv, cbuf, q) for (q, _), (cbuf, _) in zip(recvs, tmp)]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        for cbuf, buf in tmp:
+            buf.copy_(cbuf)
+
+
 def _cpu_inner(kind):
     """Oracle inner solves for TorchShard (CPU tests only)."""
     def make(a):

@@ -106,33 +106,7 @@ def test_sharded_time_step_world1_matches_single_gpu():
 
 # ---- two ranks on one GPU -------------------------------------------------------------
 def _host_staged_comm(D, dist, device):
-    class HostStagedComm(D.Comm):
-        """Test-only Comm: partial sums and halos through host memory over
-        gloo, so two ranks can share one GPU without any kernel waiting on the
-        other rank (not graph-capturable)."""
-        capturable = False
-
-        def allreduce_(self, t):
-            if self.single:
-                return t
-            c = t.detach().cpu()
-            self.dist.all_reduce(c)
-            t.copy_(c)
-            return t
-
-        def exchange(self, sends, recvs):
-            import torch
-            torch.cuda.synchronize()
-            ops = [self.dist.P2POp(self.dist.isend, buf.detach().cpu(), q) for q, buf in sends]
-            tmp = [(torch.empty(buf.numel(), dtype=buf.dtype), buf) for _, buf in recvs]
-            ops += [self.dist.P2POp(self.dist.irecv, c, q) for (q, _), (c, _) in zip(recvs, tmp)]
-            if ops:
-                for req in self.dist.batch_isend_irecv(ops):
-                    req.wait()
-            for c, buf in tmp:
-                buf.copy_(c)
-
-    return HostStagedComm(dist, device)
+    return D.HostStagedComm(dist, device)
 
 
 def _problem(name):
