@@ -1822,7 +1822,7 @@ bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, 
         p->traw, p->z2raw, zu, zv_out ? zv_out : zv_int, r, n, n + m, c);
   } else {
     dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->traw, p->z2raw, zu, n,
-                                                                          c, 0);
+                                                                          c);
   }
   LAUNCHED(ctx);
   prof_mark(ctx, 5);
@@ -2620,7 +2620,7 @@ bd_status bd_blocklu_bulk_inverse(bd_prec* p, const double* y, double* z) {
   CK(ctx, cudaMemsetAsync(c.sc + dev::S_C2, 0, sizeof(double), ctx->stream));
   CK(ctx, cudaMemsetAsync(p->z2raw, 0, sizeof(double) * n, ctx->stream));
   dev::k_combine<<<grid_for(ctx, n, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->traw, p->z2raw, z, n,
-                                                                           c, 0);
+                                                                           c);
   LAUNCHED(ctx);
   p->cnt[0] += 1;
   return BD_OK;

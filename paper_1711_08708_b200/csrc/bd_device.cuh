@@ -36,8 +36,8 @@ enum Fin {
   FIN_MEAN,         // sc[slot] = tot0 / n; sc[slot2] = sc[slot] / beta (if slot2>=0)
   FIN_DQ,           // curvature / breakdown / alpha (:101-109)
   FIN_UPDATE,       // iterations, rel, history, convergence (:114-123); mu1
-  FIN_RHO,          // rho, beta, history, max_iter stop (:95-97, :125-131)
-  FIN_RHO3,         // as FIN_RHO from (Σz_u, r_u·z_u, r_v·z_v) with z_u deflated
+  FIN_RHO3,         // rho of the deflated z from (Σz_u, r_u·z_u, r_v·z_v); beta, history,
+                    // max_iter stop (bd/krylov.py:95-97, :125-131)
   FIN_WMEAN         // mass-weighted mean (bd/system.py:145)
 };
 enum Status { ST_OK = 0, ST_ENOCONV = 3, ST_EBREAKDOWN = 4 };
@@ -197,22 +197,6 @@ __device__ void finalize(const Ctl& c, int fin, int slot, int slot2, const doubl
       }
       sc[S_MU1] = tot[1] / (double)n;
       sc[S_C1] = sc[S_MU1] / sc[S_BULK_BETA];
-      break;
-    }
-    case FIN_RHO: {
-      const double rho_next = tot[0];
-      const int k = fl[F_NPREC];
-      if (k < c.hist_cap) c.prec_hist[k] = rho_next;
-      fl[F_NPREC] = k + 1;
-      fl[F_NAPP] += 1;
-      if (fl[F_FIRST]) {
-        sc[S_BETA] = 0.0;
-        fl[F_FIRST] = 0;
-      } else {
-        sc[S_BETA] = rho_next / sc[S_RHO];
-      }
-      sc[S_RHO] = rho_next;
-      if (fl[F_ITERS] >= fl[F_MAXITER]) fl[F_STOP] = 1;
       break;
     }
     case FIN_RHO3: {

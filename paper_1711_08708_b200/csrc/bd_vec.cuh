@@ -169,27 +169,19 @@ __global__ void __launch_bounds__(TPB) k_corr_ell(LamEll L, int n, int m, const 
 }
 
 // z_u = t - bulk(corr) with both recentrings applied on the fly
-// (bd/precond.py:291-292, 311); optional sum(z_u) for the deflation mean.
+// (bd/precond.py:291-292, 311): the standalone P^{-1} (bd_blocklu_apply)
 __global__ void __launch_bounds__(TPB) k_combine(const double* __restrict__ traw,
                                                  const double* __restrict__ z2raw,
-                                                 double* __restrict__ zu, int64_t n, Ctl c,
-                                                 int with_sum) {
+                                                 double* __restrict__ zu, int64_t n, Ctl c) {
   if (inactive(c)) return;
-  __shared__ double sm[32];
   const double* sc = c.sc;
   const double mt = sc[S_MT], c1 = sc[S_C1], m2 = sc[S_M2], c2 = sc[S_C2];
-  double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double t = __dadd_rn(__dsub_rn(traw[i], mt), c1);
     const double b = __dadd_rn(__dsub_rn(z2raw[i], m2), c2);
     const double z = __dsub_rn(t, b);
     zu[i] = z;
-    acc += z;
-  }
-  if (with_sum) {
-    double v[1] = {block_sum(acc, sm)};
-    reduce_tail<1>(c, v, gridDim.x, blockIdx.x, C_COMBINE, FIN_MEAN, S_MZ, -1, n, sm);
   }
 }
 
@@ -221,23 +213,6 @@ __global__ void __launch_bounds__(TPB) k_combine_rho(const double* __restrict__ 
   v[1] = block_sum(a1, sm);
   v[2] = block_sum(a2, sm);
   reduce_tail<3>(c, v, gridDim.x, blockIdx.x, C_RHO, FIN_RHO3, 0, -1, n, sm);
-}
-
-// rho = r·z with z_u deflated on the fly (`_deflate`, bd/krylov.py:41-43;
-// `r.dot(z)`, :96 / :126)
-__global__ void __launch_bounds__(TPB) k_rho(const double* __restrict__ r, const double* __restrict__ z,
-                                             int64_t n, int64_t nm, Ctl c) {
-  if (inactive(c)) return;
-  __shared__ double sm[32];
-  const double mz = c.sc[S_MZ];
-  double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double zi = i < n ? __dsub_rn(z[i], mz) : z[i];
-    acc = fma(r[i], zi, acc);
-  }
-  double v[1] = {block_sum(acc, sm)};
-  reduce_tail<1>(c, v, gridDim.x, blockIdx.x, C_RHO, FIN_RHO, 0, -1, 0, sm);
 }
 
 // d = z_deflated + beta d (bd/krylov.py:98, 130-131); runs after the
