@@ -19,7 +19,7 @@ block-LU preconditioner (bd/precond.py:281-312), with two changes:
 The rank-local iteration is native: ``NativeShard`` holds the rank's PCG
 state and runs every vector operation, the local Λ and the block-Jacobi inner
 solves as sm_100a kernels (bd_shard_*, csrc/bd_shard.cuh) with all scalars on
-the device.  ``ShardSolver`` interleaves them with three halo exchanges and
+the device.  ``ShardSolver`` interleaves them with three halo all-gathers and
 four all-reduces per iteration (torch.distributed: NCCL over NVLink on the
 box) and captures one iteration, collectives included, in a CUDA graph.
 ``TorchShard`` restates the same kernels on CPU tensors so the CPU tests run
@@ -169,14 +169,25 @@ class Comm:
             self.dist.all_reduce(t)
         return t
 
-    def exchange(self, sends, recvs):
-        """sends / recvs: lists of (peer, contiguous tensor view), matched per
-        peer in list order (zero-length messages are left out on both sides)."""
-        ops = [self.dist.P2POp(self.dist.isend, buf, q) for q, buf in sends]
-        ops += [self.dist.P2POp(self.dist.irecv, buf, q) for q, buf in recvs]
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
+    def allgather(self, send, out):
+        """out (P x len(send), flat) <- every rank's send buffer, rank order
+        (one collective: capturable in a CUDA graph with NCCL)."""
+        if self.single:
+            out.copy_(send)
+            return out
+        if hasattr(self.dist, "all_gather_into_tensor") and send.is_cuda:
+            self.dist.all_gather_into_tensor(out, send)
+        else:
+            self.dist.all_gather(list(out.view(-1, send.numel()).unbind(0)), send)
+        return out
+
+    def allgather_object(self, obj):
+        """Setup only (host objects)."""
+        if self.single:
+            return [obj]
+        res = [None] * self.dist.get_world_size()
+        self.dist.all_gather_object(res, obj)
+        return res
 
 
 def _torch():
@@ -198,81 +209,95 @@ def order_ghosts(g: np.ndarray, m: int, part: np.ndarray) -> np.ndarray:
 
 
 class HaloPlan:
-    """Per-neighbour message layout of the three halos of an iteration: the
-    search direction d = [u | v] (all ghosts of u, heart ghosts of v) before
-    Λ, and the heart ghosts of z1 (for S_i t) and of s (for S_i s) in P^{-1}.
-    Send side: one packed buffer gathered by one kernel (bd_gather); receive
-    side: contiguous ranges of the ghost buffers (order_ghosts)."""
+    """The three halos of an iteration -- the search direction d = [u | v]
+    (every ghost of u, the heart ghosts of v) before Λ, and the heart ghosts
+    of z1 (for S_i t) and of s (for S_i s) in P^{-1} -- as ONE all-gather
+    each: every rank publishes the values of its boundary vertices (the
+    owned vertices some other rank holds as ghosts), packed by one gather
+    kernel into a buffer of the common maximal size, and unpacks its ghosts
+    from the gathered buffer with a second gather.  A collective instead of
+    point-to-point messages: capturable in the iteration's CUDA graph with
+    NCCL, and identical under gloo in the CPU tests."""
 
-    def __init__(self, lp: "LocalProblem", device, gather):
+    def __init__(self, lp: "LocalProblem", comm: Comm, device, gather):
         torch = _torch()
-        n, m = lp.n_own, lp.m_own
-        gh = lp.ghosts
-        self.n_ghost, self.m_ghost = gh.size, lp.m_ghost
         self.gather = gather
-        self.peers = sorted(set(lp.send) | set(lp.recv))
-        d_idx, h_idx = [], []
-        self.d_send, self.h_send = [], []  # (peer, offset, [lengths])
-        off_d = off_h = 0
-        for q in self.peers:
-            snd = np.asarray(lp.send.get(q, np.zeros(0, np.int64)), dtype=np.int64)
-            nh = int((snd < m).sum())
-            assert (snd[:nh] < m).all() and (snd[nh:] >= m).all(), "heart-first send order"
-            d_idx += [snd[:nh], snd[nh:], snd[:nh] + n]
-            h_idx.append(snd[:nh])
-            self.d_send.append((q, off_d, [nh, snd.size - nh, nh]))
-            self.h_send.append((q, off_h, [nh]))
-            off_d += snd.size + nh
-            off_h += nh
-        cat = lambda a: torch.as_tensor(np.concatenate(a) if a else np.zeros(0, np.int64),  # noqa: E731
-                                        dtype=torch.int64, device=device)
-        self.d_idx, self.h_idx = cat(d_idx), cat(h_idx)
-        self.d_buf = torch.zeros(max(off_d, 1), dtype=torch.float64, device=device)
-        self.h_buf = torch.zeros(max(off_h, 1), dtype=torch.float64, device=device)
-        # receive ranges: heart [h0, h1) and torso [t0, t1) of the ghost list
-        self.recv = {}
-        for q in self.peers:
-            slots = np.asarray(lp.recv.get(q, np.zeros(0, np.int64)), dtype=np.int64)
-            hs, ts = slots[slots < lp.m_ghost], slots[slots >= lp.m_ghost]
-            for s in (hs, ts):
-                assert s.size == 0 or np.array_equal(s, np.arange(s[0], s[0] + s.size)), \
-                    "ghosts not grouped by owner"
-            self.recv[q] = ((int(hs[0]) if hs.size else 0, hs.size),
-                            (int(ts[0]) if ts.size else 0, ts.size))
-        self.ug = torch.zeros(max(self.n_ghost, 1), dtype=torch.float64, device=device)
-        self.vg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
-        self.tg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
-        self.sg = torch.zeros(max(self.m_ghost, 1), dtype=torch.float64, device=device)
+        self.comm = comm
+        self.n_ghost, self.m_ghost = lp.ghosts.size, lp.m_ghost
+        f64 = dict(dtype=torch.float64, device=device)
+        self.ug = torch.zeros(max(self.n_ghost, 1), **f64)
+        self.vg = torch.zeros(max(self.m_ghost, 1), **f64)
+        self.tg = torch.zeros(max(self.m_ghost, 1), **f64)
+        self.sg = torch.zeros(max(self.m_ghost, 1), **f64)
+        self.active = not comm.single and (lp.ghosts.size > 0 or any(len(v) for v in lp.send.values()))
+        m_glob = lp.m_global
+        snd = [np.asarray(v, dtype=np.int64) for v in lp.send.values()]
+        loc = np.unique(np.concatenate(snd)) if snd else np.zeros(0, np.int64)
+        b_glob = lp.owned[loc]
+        order = np.argsort(b_glob)
+        b_glob, loc = b_glob[order], loc[order]
+        allb = comm.allgather_object(b_glob)
+        self.active = not comm.single
+        if not self.active:
+            return
+        bh = [b[b < m_glob] for b in allb]
+        self.maxb = max(1, max(b.size for b in allb))
+        self.maxbh = max(1, max(b.size for b in bh))
+        hm = b_glob < m_glob
+        # pack: [u(B_r) | pad][v(Bh_r) | pad] from d = [u | v]; heart-only halos
+        # from a heart vector: [x(Bh_r) | pad]
+        pd = np.zeros(self.maxb + self.maxbh, dtype=np.int64)
+        pd[: loc.size] = loc
+        pd[self.maxb: self.maxb + int(hm.sum())] = lp.n_own + loc[hm]  # heart rows lead the owned
+        ph = np.zeros(self.maxbh, dtype=np.int64)
+        ph[: int(hm.sum())] = loc[hm]
+        # unpack: ghost g owned by rank q
+        gh = lp.ghosts
+        owner = np.empty(gh.size, dtype=np.int64)
+        pos = np.empty(gh.size, dtype=np.int64)
+        posh = np.zeros(gh.size, dtype=np.int64)
+        part = getattr(lp, "ghost_owner", None)
+        for q in range(len(allb)):
+            if q == lp.rank:
+                continue
+            sel = np.isin(gh, allb[q]) if part is None else (part == q)
+            if not sel.any():
+                continue
+            owner[sel] = q
+            pos[sel] = np.searchsorted(allb[q], gh[sel])
+            hsel = sel & (gh < m_glob)
+            posh[hsel] = np.searchsorted(bh[q], gh[hsel])
+        w = self.maxb + self.maxbh
+        ud = owner * w + pos
+        vd = owner[: lp.m_ghost] * w + self.maxb + posh[: lp.m_ghost]
+        hh = owner[: lp.m_ghost] * self.maxbh + posh[: lp.m_ghost]
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=device)  # noqa: E731
+        self.pack_d, self.pack_h = T(pd), T(ph)
+        self.unpack_u, self.unpack_v, self.unpack_h = T(ud), T(vd), T(hh)
+        P = len(allb)
+        self.send_d = torch.zeros(w, **f64)
+        self.recv_d = torch.zeros(P * w, **f64)
+        self.send_h = torch.zeros(self.maxbh, **f64)
+        self.recv_h = torch.zeros(P * self.maxbh, **f64)
 
     def halo_d(self, comm, src):
         """ug, vg <- ghosts of u and heart ghosts of v of the block vector src."""
-        if not self.peers:
+        if not self.active:
             return
-        self.gather(self.d_idx, src, self.d_buf)
-        sends, recvs = [], []
-        for q, off, lens in self.d_send:
-            for ln in lens:
-                if ln:
-                    sends.append((q, self.d_buf[off: off + ln]))
-                off += ln
-        for q in self.peers:
-            (h0, hn), (t0, tn) = self.recv[q]
-            if hn:
-                recvs.append((q, self.ug[h0: h0 + hn]))
-            if tn:
-                recvs.append((q, self.ug[t0: t0 + tn]))
-            if hn:
-                recvs.append((q, self.vg[h0: h0 + hn]))
-        comm.exchange(sends, recvs)
+        self.gather(self.pack_d, src, self.send_d)
+        comm.allgather(self.send_d, self.recv_d)
+        self.gather(self.unpack_u, self.recv_d, self.ug)
+        if self.m_ghost:
+            self.gather(self.unpack_v, self.recv_d, self.vg)
 
     def halo_h(self, comm, src, dst):
         """dst <- heart ghosts of the heart-block vector src."""
-        if not self.peers:
+        if not self.active:
             return
-        self.gather(self.h_idx, src, self.h_buf)
-        sends = [(q, self.h_buf[off: off + lens[0]]) for q, off, lens in self.h_send if lens[0]]
-        recvs = [(q, dst[h0: h0 + hn]) for q in self.peers for (h0, hn), _ in [self.recv[q]] if hn]
-        comm.exchange(sends, recvs)
+        self.gather(self.pack_h, src, self.send_h)
+        comm.allgather(self.send_h, self.recv_h)
+        if self.m_ghost:
+            self.gather(self.unpack_h, self.recv_h, dst)
 
 
 # ---- the rank-local iteration: native (sm_100a) and a CPU restatement ----------------
@@ -608,7 +633,7 @@ class TorchShard:
 
 class ShardSolver:
     """The sharded deflated PCG (bd/krylov.py:46-140, block-Jacobi block-LU
-    preconditioner bd/precond.py:281-312) of one rank: halo exchanges and the
+    preconditioner bd/precond.py:281-312) of one rank: halo all-gathers and the
     four all-reduces per iteration around the rank-local kernels of `ops`
     (NativeShard on the box, TorchShard in the CPU tests).  On a CUDA device
     one iteration, collectives included, is captured into a CUDA graph and
@@ -617,7 +642,7 @@ class ShardSolver:
 
     def __init__(self, lp: "LocalProblem", comm: Comm, ops):
         self.lp, self.comm, self.ops = lp, comm, ops
-        self.plan = HaloPlan(lp, ops.device, ops.gather)
+        self.plan = HaloPlan(lp, comm, ops.device, ops.gather)
         self.msum = comm.allreduce([float(np.sum(lp.mass))])[0]
         self.graph = None
         self._graph_key = None
@@ -754,18 +779,15 @@ class HostStagedComm(Comm):
         t.copy_(c)
         return t
 
-    def exchange(self, sends, recvs):
-        torch = _torch()
-        if sends or recvs:
-            torch.cuda.synchronize()
-        ops = [self.dist.P2POp(self.dist.isend, buf.detach().cpu(), q) for q, buf in sends]
-        tmp = [(torch.empty(buf.numel(), dtype=buf.dtype), buf) for _, buf in recvs]
-        ops += [self.dist.P2POp(self.dist.irecv, cbuf, q) for (q, _), (cbuf, _) in zip(recvs, tmp)]
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
-        for cbuf, buf in tmp:
-            buf.copy_(cbuf)
+    def allgather(self, send, out):
+        if self.single:
+            out.copy_(send)
+            return out
+        c = send.detach().cpu()
+        parts = [_torch().empty_like(c) for _ in range(self.dist.get_world_size())]
+        self.dist.all_gather(parts, c)
+        out.copy_(_torch().cat(parts))
+        return out
 
 
 def _cpu_inner(kind):
