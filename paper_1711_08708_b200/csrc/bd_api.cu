@@ -173,6 +173,7 @@ struct DevBTile {
 };
 
 struct DevSuper {
+  int dchunk = 16;           // rows per dense-phase slice (BD_SUPER_DCHUNK)
   double* pinv = nullptr;    // panel inverses of the big supernodes' dense blocks
   int* sn_pan = nullptr;
   int* task_kind = nullptr;  // forward: split external phases (nullptr: none)
@@ -643,6 +644,16 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
       for (int64_t q = L.indptr[i]; q < L.indptr[i + 1]; ++q)
         if (L.indices[q] < start[sn]) ++extb[sn_of[L.indices[q]]];
   const int64_t split_min = getenv("BD_SUPER_SPLIT") ? atoll(getenv("BD_SUPER_SPLIT")) : 8192;
+  // whole-block inverses from this many rows (used below and by the dense-phase split)
+  const int64_t inv_min = getenv("BD_SUPER_INV_MIN") ? atoll(getenv("BD_SUPER_INV_MIN")) : 128;
+  // split the dense GEMV of supernodes of at least this many rows (0: never)
+  const int64_t dsplit_min_env = getenv("BD_SUPER_DSPLIT") ? atoll(getenv("BD_SUPER_DSPLIT")) : 128;
+  const int64_t dsplit_min = dsplit_min_env > 0 ? dsplit_min_env : (int64_t)1 << 40;
+  // (config 1, ms per step: 16 rows 8.72, 32 8.90, 64 9.16, 128 9.50; no
+  // slicing 12.45: profiles/r02_cfg1_relax_sweep.txt)
+  const int dch = std::max(16, std::min(256, getenv("BD_SUPER_DCHUNK") ? atoi(getenv("BD_SUPER_DCHUNK"))
+                                                                       : 16));
+  fw->dchunk = bw->dchunk = dch;
   // dense block of supernode sn: D[k][j] (j <= k) = L[start+k][start+j], the
   // last k+1 entries of the row (diagonal last)
   auto dense = [&](int64_t c0, int64_t k, int64_t j) -> long double {
@@ -686,9 +697,23 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
             kind.push_back(1);
             arg.push_back(ch * dev::SN_CHUNK);
           }
-          tasks.push_back((int32_t)k);
-          kind.push_back(2);
-          arg.push_back(nch);
+          // the dense phase: one task, or (big supernodes with a whole-block
+          // inverse) DCH-row slices of its GEMV spread over several CTAs
+          // (kind 3: arg = ext chunks | slice << 8 | slices << 16)
+          const int nd = (inv_min > 0 && sz[k] >= inv_min && sz[k] >= dsplit_min)
+                             ? (int)((sz[k] + dch - 1) / dch)
+                             : 0;
+          if (nd > 1) {
+            for (int q = 0; q < nd; ++q) {
+              tasks.push_back((int32_t)k);
+              kind.push_back(3);
+              arg.push_back(nch | (q << 8) | (nd << 16));
+            }
+          } else {
+            tasks.push_back((int32_t)k);
+            kind.push_back(2);
+            arg.push_back(nch);
+          }
           any_split = true;
         } else {
           tasks.push_back((int32_t)k);
@@ -752,7 +777,6 @@ bd_status build_super(bd_ctx* ctx, const HostCsr& L, DevSuper* fw, DevSuper* bw)
     // supernodes of at least BD_SUPER_INV_MIN rows: their dense phase becomes
     // one GEMV instead of ns/32 dependent panel steps
     {
-      const int64_t inv_min = getenv("BD_SUPER_INV_MIN") ? atoll(getenv("BD_SUPER_INV_MIN")) : 128;
       std::vector<long long> off(ns, -1);
       long long tot = 0;
       std::vector<int64_t> which;
@@ -1567,7 +1591,8 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tl{(int)p->n,        p->L.rowptr,  p->L.col,    p->L.val, p->SL.sn_start,
                      p->SL.sn_size,     p->SL.task_sn, p->SL.ntasks, nullptr,
                      p->SL.task_kind,   p->SL.task_arg, p->SL.sn_cnt, p->rext,
-                     p->SL.pinv,        p->SL.sn_pan,  p->SL.task_w, p->SL.sinv, p->SL.sn_inv};
+                     p->SL.pinv,        p->SL.sn_pan,  p->SL.task_w, p->SL.sinv, p->SL.sn_inv,
+                     p->SL.dchunk};
     dev::k_trsv_super<true, Rhs><<<p->SL.grid, 512, 0, st>>>(tl, rhs, p->y_int, nullptr, c, ctr0,
                                                               ctr0 + 1);
     LAUNCHED(ctx);
@@ -1576,7 +1601,8 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     dev::SuperTri tu{(int)p->n,        p->U.rowptr,  p->U.col,    p->U.val, p->SU.sn_start,
                      p->SU.sn_size,     p->SU.task_sn, p->SU.ntasks, p->perm,
                      p->SU.task_kind,   p->SU.task_arg, p->SU.sn_cnt, p->rext,
-                     p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w, p->SU.sinv, p->SU.sn_inv};
+                     p->SU.pinv,        p->SU.sn_pan,  p->SU.task_w, p->SU.sinv, p->SU.sn_inv,
+                     p->SU.dchunk};
     dev::k_trsv_super<false, dev::RhsGather><<<p->SU.grid, 512, 0, st>>>(
         tu, dev::RhsGather{p->y_int}, x_int, out, c, ctr0 + 2, ctr0 + 3);
     LAUNCHED(ctx);
@@ -2299,7 +2325,7 @@ bd_status bd_inner_create_ex(bd_ctx* ctx, int kind, int64_t n, const int64_t* in
     // frac 0.85 uncapped 13.7, frac 0.9 with blocks capped at 320 rows 12.5,
     // frac 1.0 uncapped 1188; nnz(L) +18 %)
     const double relax = getenv("BD_SUPER_RELAX") ? atof(getenv("BD_SUPER_RELAX")) : 0.9;
-    const int relax_max = getenv("BD_SUPER_RELAX_MAX") ? atoi(getenv("BD_SUPER_RELAX_MAX")) : 320;
+    const int relax_max = getenv("BD_SUPER_RELAX_MAX") ? atoi(getenv("BD_SUPER_RELAX_MAX")) : dev::SN_MAX;
     if (relax > 0.0) relax_supernodes(&lower, relax, std::min(relax_max, dev::SN_MAX));
   }
   HostCsr upper = transpose(lower);

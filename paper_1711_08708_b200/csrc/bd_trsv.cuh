@@ -1758,6 +1758,7 @@ struct SuperTri {
   // starting at sn_inv[supernode] (-1: panels)
   const double* sinv;
   const long long* sn_inv;
+  int dchunk;  // rows per dense-phase slice (kind-3 tasks)
 };
 
 constexpr int SN_MAX = 1024;
@@ -1944,6 +1945,41 @@ __global__ void __launch_bounds__(512, 2) k_trsv_super(SuperTri t, Rhs rhs, doub
       if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(t.sn_cnt + s0, 1);
+      }
+      continue;
+    }
+    if (kind == 3) {
+      // one slice of a big supernode's dense phase through its whole-block
+      // inverse: wait for the supernode's external-phase chunks (y in rext),
+      // then rows [l0, l1) of x = X y, published as they complete
+      const int a = t.task_arg[task], nch = a & 0xff, part = (a >> 8) & 0xff, nparts = a >> 16;
+      const int c0 = t.sn_start[s0], ns = t.sn_size[s0];
+      if (threadIdx.x == 0) {
+        const volatile int* cnt = t.sn_cnt + s0;
+        while (*cnt < nch) __nanosleep(64);
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < ns; k += blockDim.x) r[k] = ld_relaxed_if(&t.rext[c0 + k], true);
+      __syncthreads();
+      const double* X = t.sinv + t.sn_inv[s0];
+      const int l0 = part * t.dchunk, l1 = min(ns, l0 + t.dchunk);
+      for (int l = l0 + warp; l < l1; l += nw) {
+        const double* xr = X + (long long)l * (l + 1) / 2;
+        double acc = 0.0;
+        for (int m = lane; m <= l; m += 32) acc = fma(__ldg(&xr[m]), r[LOWER ? m : ns - 1 - m], acc);
+        const double v = group_sum<32>(acc);
+        if (lane == 0) {
+          const int i = c0 + (LOWER ? l : ns - 1 - l);
+          publish(&x[i], v);
+          if (out) out[t.perm ? t.perm[i] : i] = v;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        // the last slice resets the counter for the next pass (every slice
+        // has passed its wait once all of them have counted in)
+        if (atomicAdd(t.sn_cnt + s0, 1) == nch + nparts - 1) t.sn_cnt[s0] = 0;
       }
       continue;
     }
