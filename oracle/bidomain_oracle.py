@@ -187,6 +187,9 @@ def _c_lib():
         lib.oracle_ic0.restype = ctypes.c_int
         lib.oracle_ic0.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_int,
                                                                                ctypes.c_void_p]
+        for f in (lib.oracle_trsv_lower, lib.oracle_trsv_upper):
+            f.restype = None
+            f.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 6
         _clib = lib
     return _clib
 
@@ -207,15 +210,39 @@ def ic0_factor(a, max_restarts=20):
     return sp.csr_matrix((out, low.indices.copy(), low.indptr.copy()), shape=(n, n)), got
 
 
-class InnerIC0:
-    """precond.py:123-198 (apply: spsolve_triangular lower then upper)."""
+def _trsv_c(fn, a, y):
+    """C restatement of one spsolve_triangular call (bit-identical; ic0_oracle.c)."""
+    n = a.shape[0]
+    ip = np.ascontiguousarray(a.indptr, dtype=np.int64)
+    ci = np.ascontiguousarray(a.indices, dtype=np.int32)
+    val = np.ascontiguousarray(a.data, dtype=np.float64)
+    b = np.ascontiguousarray(y, dtype=np.float64)
+    x = np.empty(n)
+    work = np.empty(n)
+    fn(n, ip.ctypes.data, ci.ctypes.data, val.ctypes.data, b.ctypes.data, x.ctypes.data,
+       work.ctypes.data)
+    return x
 
-    def __init__(self, a, max_restarts=20, python=False):
+
+class InnerIC0:
+    """precond.py:123-198 (apply: spsolve_triangular lower then upper).
+
+    ``fast_apply=True`` runs the two triangular solves through the C
+    restatement of scipy's spsolve_triangular arithmetic (``oracle_trsv_*``,
+    bit-identical, ~10x faster); the default keeps the scipy calls the
+    reference makes, so timing the oracle times the reference's own cost."""
+
+    def __init__(self, a, max_restarts=20, python=False, fast_apply=False):
         f = ic0_factor_py if python else ic0_factor
         self.lower, self.restarts_used = f(a, max_restarts)
         self.upper = self.lower.T.tocsr()
+        self.fast_apply = fast_apply
 
     def apply(self, y):
+        if self.fast_apply:
+            lib = _c_lib()
+            z = _trsv_c(lib.oracle_trsv_lower, self.lower, y)
+            return _trsv_c(lib.oracle_trsv_upper, self.upper, z)
         z = spla.spsolve_triangular(self.lower, np.asarray(y, dtype=float), lower=True)
         return spla.spsolve_triangular(self.upper, z, lower=False)
 
@@ -247,9 +274,9 @@ class InnerExact:
         return self.lu.solve(np.asarray(y, dtype=float))
 
 
-def make_inner(name, a):
+def make_inner(name, a, fast_apply=False):
     if name == "ic0":
-        return InnerIC0(a)
+        return InnerIC0(a, fast_apply=fast_apply)
     if name == "jacobi":
         return InnerJacobi(a)
     if name == "exact":
@@ -260,12 +287,12 @@ def make_inner(name, a):
 class BlockLU:
     """precond.py:246-312 (P_Λ with the monodomain K_m)."""
 
-    def __init__(self, S1, Si, Km, inner="exact"):
+    def __init__(self, S1, Si, Km, inner="exact", fast_apply=False):
         self.Si = sp.csr_matrix(Si)
         self.n, self.m = S1.shape[0], Si.shape[0]
         self.beta, grounded = regularize(S1)
-        self.bulk = make_inner(inner, grounded)
-        self.schur = make_inner(inner, Km)
+        self.bulk = make_inner(inner, grounded, fast_apply)
+        self.schur = make_inner(inner, Km, fast_apply)
         self.p1 = self.pk = self.si = 0
 
     def bulk_inverse(self, y):

@@ -64,3 +64,48 @@ int oracle_ic0(int64_t n, const int64_t* ip, const int32_t* ci, const double* da
   }
   return -1;
 }
+
+/* IC(0) apply, IncompleteCholesky0.apply_inverse (precond.py:191-194):
+ * scipy.sparse.linalg.spsolve_triangular(L, y, lower=True) then
+ * spsolve_triangular(L^T, z, lower=False), restated in the arithmetic order of
+ * scipy 1.18 (linsolve.py spsolve_triangular -> SuperLU gstrs, trans='T'):
+ *
+ * lower (CSR L, diagonal last in each row): the strictly lower entries are
+ * scaled by the inverse diagonal of their column, a unit-lower solve runs in
+ * column order with each row's products subtracted one by one, and the result
+ * is multiplied by the inverse diagonal:
+ *   y_i = b_i - sum_{j<i} (L_ij * (1/L_jj)) * y_j (ascending j),  x = y * (1/L_ii).
+ * upper (CSR U = L^T, diagonal first): the right-hand side is first divided by
+ * the scaled diagonal U_ii * (1/U_ii), then a unit-upper back substitution,
+ * then the multiplication by the inverse diagonal.
+ * Output is bit-identical to the scipy calls (tests/test_oracle_golden.py). */
+void oracle_trsv_lower(int64_t n, const int64_t* ip, const int32_t* ci, const double* val,
+                       const double* b, double* x, double* work) {
+  double* inv = work;
+  for (int64_t i = 0; i < n; i++) inv[i] = 1.0 / val[ip[i + 1] - 1];
+  for (int64_t i = 0; i < n; i++) {
+    double s = b[i];
+    for (int64_t k = ip[i]; k < ip[i + 1] - 1; k++) {
+      int32_t j = ci[k];
+      s = s - x[j] * (val[k] * inv[j]);
+    }
+    x[i] = s;
+  }
+  for (int64_t i = 0; i < n; i++) x[i] = x[i] * inv[i];
+}
+
+void oracle_trsv_upper(int64_t n, const int64_t* ip, const int32_t* ci, const double* val,
+                       const double* b, double* x, double* work) {
+  double* inv = work;
+  for (int64_t i = 0; i < n; i++) inv[i] = 1.0 / val[ip[i]];
+  for (int64_t i = 0; i < n; i++) x[i] = b[i] / (val[ip[i]] * inv[i]);
+  for (int64_t i = n - 1; i >= 0; i--) {
+    double s = x[i];
+    for (int64_t k = ip[i] + 1; k < ip[i + 1]; k++) {
+      int32_t j = ci[k];
+      s = s - x[j] * (val[k] * inv[j]);
+    }
+    x[i] = s;
+  }
+  for (int64_t i = 0; i < n; i++) x[i] = x[i] * inv[i];
+}

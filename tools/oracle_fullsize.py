@@ -54,6 +54,9 @@ def main():
     ap.add_argument("--sub-stride", type=int, default=29)
     ap.add_argument("--sub-steps", default="1,2,3,5,10,20,30,40,41,45,50,100,150,200")
     ap.add_argument("--proj-k", type=int, default=32)
+    ap.add_argument("--scipy-trsv", action="store_true",
+                    help="IC(0) apply through scipy's spsolve_triangular instead of its "
+                         "bit-identical C restatement (oracle_trsv_*; ~10x slower)")
     a = ap.parse_args()
     t0 = time.perf_counter()
     wl = configs.BUILDERS[a.config](a.cells) if a.cells else configs.BUILDERS[a.config]()
@@ -62,7 +65,8 @@ def main():
     km = build_monodomain_matrix(wl.mesh, wl.params, sysm.gamma, wl.fibers)
     t_asm = time.perf_counter() - t0
     t0 = time.perf_counter()
-    pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, inner)
+    pre = orc.BlockLU(sysm.stiff_total, sysm.stiff_intra, km, inner,
+                      fast_apply=not a.scipy_trsv)
     t_setup = time.perf_counter() - t0
     tag = f"{a.config}_{a.cells}" if a.cells else a.config
     out_path = a.out or os.path.join(REPO, "tests", "golden", f"{tag}_{inner}_oracle.json")
