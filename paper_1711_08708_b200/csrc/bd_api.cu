@@ -165,10 +165,14 @@ struct DevBTile {
   bool reg = false;       // k_trsv_rtile instead of k_trsv_btile
   bool tile_rhs = false;  // k_trsv_rtile with the right-hand side pre-gathered in tile order
   bool reg_smem = false;  // k_trsv_rtile with the inverse staged in shared memory
+  bool rpipe = false;     // k_trsv_rpipe: packed per-tile records through a TMA ring
+  unsigned char* rec = nullptr;
+  int recb = 0, depth = 2;
   dev::BTileDev dev() const {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
                          ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
-                         prefetch, poll_depth, inbox,    dst,      dmax,     exw};
+                         prefetch, poll_depth, inbox,    dst,      dmax,     exw,
+                         rec,     recb,     depth};
   }
 };
 
@@ -1201,6 +1205,47 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       CK(ctx, cudaFuncSetAttribute(dev::k_trsv_ptile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)out->smem));
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
+    } else if (kn == "rpipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) {
+      // one packed record per tile (dev::rp_layout), fetched by one TMA bulk copy
+      const dev::RpLayout lay = dev::rp_layout(rs, xs, (int)is, es, rps);
+      std::vector<unsigned char> rec((size_t)nt * lay.bytes, 0);
+#pragma omp parallel for schedule(static)
+      for (int t = 0; t < nt; ++t) {
+        unsigned char* r = rec.data() + (size_t)t * lay.bytes;
+        std::memcpy(r, &nr[t], 4);
+        std::memcpy(r + lay.o_row, &row[(size_t)t * rs], 4 * (size_t)rs);
+        std::memcpy(r + lay.o_in, &in[(size_t)t * xs], 4 * (size_t)xs);
+        std::memcpy(r + lay.o_rp, &rp[(size_t)t * rps], 2 * (size_t)rps);
+        std::memcpy(r + lay.o_slot, &slot[(size_t)t * es], 2 * (size_t)es);
+        std::memcpy(r + lay.o_val, &val[(size_t)t * es], 8 * (size_t)es);
+        std::memcpy(r + lay.o_inv, &inv[(size_t)t * is], 8 * (size_t)is);
+      }
+      CK(ctx, upload_vec(&out->rec, rec));
+      out->recb = lay.bytes;
+      out->depth = std::max(2, std::min(8, getenv("BD_RPIPE_DEPTH") ? atoi(getenv("BD_RPIPE_DEPTH")) : 2));
+      out->reg = true;
+      out->rpipe = true;
+      out->threads = 256;
+      out->smem = dev::rp_smem(out->recb, out->depth, xs);
+      auto pg = dev::k_trsv_rpipe<dev::RhsGather>;
+      auto pv = dev::k_trsv_rpipe<dev::RhsVec>;
+      auto ps = dev::k_trsv_rpipe<dev::RhsSchur>;
+      {
+        static std::mutex mu2;
+        static size_t attr2[64] = {};
+        int dev_id = 0;
+        CK(ctx, cudaGetDevice(&dev_id));
+        std::lock_guard<std::mutex> lk(mu2);
+        size_t& cur = attr2[dev_id & 63];
+        if (out->smem > cur) {
+          const int sm = (int)out->smem;
+          CK(ctx, cudaFuncSetAttribute(pg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(pv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(ps, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          cur = out->smem;
+        }
+      }
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ps, 256, out->smem);
     } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) {
       out->reg = true;
       out->reg_smem = kn == "rsmem";
@@ -1224,6 +1269,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
 }
 
 void free_btile(DevBTile* d) {
+  cudaFree(d->rec);
   cudaFree(d->dst);
   cudaFree(d->opos);
   cudaFree(d->tile_nr);
@@ -1387,7 +1433,10 @@ bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* x
                        int ctr_task, int ctr_done, double* reset, double* r0 = nullptr,
                        double* r1 = nullptr) {
   bd_ctx* ctx = p->ctx;
-  if (b.reg && b.reg_smem && !reset)
+  if (b.rpipe && !reset)
+    dev::k_trsv_rpipe<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+                                                                       ctr_done, r0, r1);
+  else if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
         b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else if (b.reg && !reset)

@@ -917,6 +917,11 @@ struct BTileDev {
   const int* dst;                   // [tile][rs][dmax] inbox slots fed by each row (-1 pad)
   int dmax;                         // <= 8
   int exw;                          // max external entries of a row (k_trsv_rtile: <= 16)
+  // k_trsv_rpipe: one packed record per tile (see rp_layout), fetched with a
+  // single 1D TMA bulk copy into a ring of `depth` shared-memory slots
+  const unsigned char* rec;
+  int recb;                         // record stride in bytes (16-byte multiple)
+  int depth;                        // ring slots per CTA (>= 2)
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
@@ -1341,6 +1346,221 @@ __global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
         publish(&xg[row], x);
         if (kTileRhs && op >= 0) bt_next[op] = x;
       }
+    }
+    if (trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[8 * t + 7] = gtimer();
+      trace[8 * t + 2] = gtimer();
+      trace[8 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    const unsigned d = atomicAdd(&c.ctr[ctr_done], 1u);
+    last_s = (d == gridDim.x - 1u);
+  }
+  __syncthreads();
+  if (last_s && tid == 0) {
+    c.ctr[ctr_task] = 0u;
+    c.ctr[ctr_done] = 0u;
+    __threadfence();
+  }
+}
+
+// ---- register tiles fed by a TMA ring -----------------------------------------
+// k_trsv_rtile's arithmetic (same thread mapping, same sums in the same order,
+// so the results are bit-identical) with the tile's preparation taken off the
+// CTA's serial path.  Every array of a tile is packed into ONE record
+// (rp_layout: header, rows, inputs, entry ranges / slots / values, inverse), so
+// a tile is fetched by a single cp.async.bulk into a shared-memory ring slot,
+// completion signalled on the slot's mbarrier.  The CTA holds `depth` tiles:
+// it works on the oldest while the others' records are in flight.  Thread 0
+// fires the atomic grab for the slot's refill at the top of an iteration and
+// consumes it after the tile's second barrier, when the slot is free again, so
+// neither the grab's round trip nor the record's DRAM latency sits between two
+// tiles.  When a record has landed the inverse goes smem -> registers while the
+// first poll loads are already in flight.  Deadlock-free like the other
+// in-order grabbers: a CTA finishes its tiles in grab order, so the smallest
+// unfinished tile is always some CTA's current one.
+struct RpLayout {
+  int o_row, o_in, o_rp, o_slot, o_val, o_inv, bytes;
+};
+__host__ __device__ inline RpLayout rp_layout(int rs, int xs, int is, int es, int rps) {
+  RpLayout l;
+  l.o_row = 16;                 // header: int nr, 3 x pad
+  l.o_in = l.o_row + 4 * rs;
+  l.o_rp = l.o_in + 4 * xs;
+  l.o_slot = l.o_rp + 2 * rps;
+  l.o_val = l.o_slot + 2 * es;
+  l.o_inv = l.o_val + 8 * es;
+  l.bytes = (l.o_inv + 8 * is + 15) & ~15;
+  return l;
+}
+// shared memory: ring [depth][recb] | ys | xin (+zero slot) | mbarriers | tile ids
+__host__ __device__ inline size_t rp_smem(int recb, int depth, int xs) {
+  return (size_t)depth * recb + sizeof(double) * ((size_t)RT_ROWS + xs + 2) + 8 * (size_t)depth +
+         4 * (size_t)((depth + 3) & ~3);
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// one elected thread: arm the slot's barrier with the byte count and start the copy
+__device__ __forceinline__ void tma_fetch(void* dst, const void* src, unsigned bytes, void* bar) {
+  const unsigned b = smem_u32(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+template <class Rhs>
+__global__ void __launch_bounds__(256, 4)
+    k_trsv_rpipe(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
+                 double* reset0 = nullptr, double* reset1 = nullptr) {
+  if (inactive(c)) return;
+  extern __shared__ __align__(128) unsigned char rp_sm[];
+  const int D = T.depth;
+  const RpLayout lay = rp_layout(T.rs, T.xs, T.is, T.es, T.rps);
+  double* ys = reinterpret_cast<double*>(rp_sm + (size_t)D * T.recb);  // RT_ROWS
+  double* xin = ys + RT_ROWS;                                          // xs inputs, xin[xs] = 0
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(xin + T.xs + 2);
+  int* ids = reinterpret_cast<int*>(mbar + D);
+  __shared__ int last_s;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int k = warp * 8 + (lane >> 2);  // row slot
+  const int g = lane & 3;                // column group
+  const int jmax = (8 * warp + 7) >> 2;  // warp-uniform: columns beyond the warp's rows are zero
+  unsigned long long* trace = g_tile_trace;
+  if (tid == 0) {
+    xin[T.xs] = 0.0;
+    for (int s = 0; s < D; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int s = 0; s < D; ++s) {
+      const int t = (int)atomicAdd(&c.ctr[ctr_task], 1u);
+      ids[s] = t;
+      if (t < T.ntiles) {
+        tma_fetch(rp_sm + (size_t)s * T.recb, T.rec + (size_t)t * T.recb, (unsigned)T.recb, &mbar[s]);
+        if (trace) trace[8 * t] = gtimer();
+      }
+    }
+  }
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int s = it % D;
+    const int t = ids[s];
+    if (t >= T.ntiles) break;
+    unsigned nxt = 0;
+    if (tid == 0) nxt = atomicAdd(&c.ctr[ctr_task], 1u);  // the slot's refill; used after barrier 2
+    const unsigned char* buf = rp_sm + (size_t)s * T.recb;
+    mbar_wait(&mbar[s], (unsigned)(it / D) & 1u);
+    const int nr = *reinterpret_cast<const int*>(buf);
+    const int* rowa = reinterpret_cast<const int*>(buf + lay.o_row);
+    const int* ina = reinterpret_cast<const int*>(buf + lay.o_in);
+    const unsigned short* erp = reinterpret_cast<const unsigned short*>(buf + lay.o_rp);
+    const unsigned short* esl = reinterpret_cast<const unsigned short*>(buf + lay.o_slot);
+    const double* ev = reinterpret_cast<const double*>(buf + lay.o_val);
+    const double* ib = reinterpret_cast<const double*>(buf + lay.o_inv);
+    const int row = k < nr ? rowa[k] : -1;
+    // the tile's distinct inputs, one poller each: first loads go out now
+    int icol[2];
+    long long pv[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * nth;
+      icol[h] = j < T.xs ? ina[j] : -1;
+      if (icol[h] >= 0)
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(pv[h]) : "l"(&xg[icol[h]]) : "memory");
+    }
+    double b;
+    if constexpr (Rhs::kScalar) {
+      b = rhs.template eval<1>(row, 0);
+    } else {
+      b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
+    }
+    // inverse entries inv[k][g+4j] (packed column-major: column l = rows l..nr-1
+    // at l*nr - l(l-1)/2) from the ring slot into registers
+    double a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int l = g + 4 * j;
+      const bool ok = (j <= jmax) && l <= k && k < nr;
+      const int idx = ok ? l * nr - ((l * (l - 1)) >> 1) + (k - l) : 0;
+      const double v = ib[idx];
+      a[j] = ok ? v : 0.0;
+    }
+    if (g == 0 && row >= 0) {  // sentinel resets folded into the pass (BD_FOLD_FILL)
+      if (reset0) reset0[row] = __longlong_as_double(SENTINEL);
+      if (reset1) reset1[row] = __longlong_as_double(SENTINEL);
+    }
+    if (trace && tid == 0) trace[8 * t + 5] = gtimer();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (icol[h] < 0) continue;
+      const double* pj = &xg[icol[h]];
+      long long v = pv[h];
+      while (v == SENTINEL)
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(pj) : "memory");
+      xin[tid + h * nth] = __longlong_as_double(v);
+    }
+    __syncthreads();  // barrier 1: inputs in shared memory
+    if (trace && tid == 0) trace[8 * t + 4] = gtimer();
+    {
+      const int kc = k < nr ? k : 0;
+      const int e0 = erp[kc], e1 = k < nr ? erp[kc + 1] : e0;
+      double acc = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        if (h >= 2 && 4 * h >= T.exw) break;  // rows with > 8 entries: heart-first torso rows
+        const int e = e0 + g + 4 * h;
+        const bool ok = e < e1;
+        const int ei = ok ? e : 0;
+        const int sl = ok ? (int)esl[ei] : T.xs;
+        acc = fma(ev[ei], xin[sl], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (g == 0) ys[k] = row >= 0 ? __dsub_rn(b, acc) : 0.0;
+    }
+    if (trace && tid == 0) trace[8 * t + 6] = gtimer();
+    __syncthreads();  // barrier 2: y in shared memory; the ring slot is free
+    if (trace && tid == 0) trace[8 * t + 1] = gtimer();
+    if (tid == 0) {
+      ids[s] = (int)nxt;  // read at the top of iteration it + D (D >= 2: a barrier in between)
+      if ((int)nxt < T.ntiles) {
+        tma_fetch(rp_sm + (size_t)s * T.recb, T.rec + (size_t)nxt * T.recb, (unsigned)T.recb, &mbar[s]);
+        if (trace) trace[8 * (size_t)nxt] = gtimer();
+      }
+    }
+    {
+      double sm[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j <= jmax) sm[j & 3] = fma(a[j], ys[g + 4 * j], sm[j & 3]);
+      double x = (sm[0] + sm[1]) + (sm[2] + sm[3]);
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      x += __shfl_xor_sync(0xffffffffu, x, 2);
+      if (g == 0 && row >= 0) publish(&xg[row], x);
     }
     if (trace && tid == 0) {
       unsigned smid;

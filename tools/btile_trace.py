@@ -85,4 +85,23 @@ for rep in range(reps):
     seg = np.array_split(np.arange(len(path)), 6)
     print("   path poll/cp by segment:", [(round(p_poll[s_].mean(), 2), round(p_cp[s_].mean(), 2)) for s_ in seg])
     print("   path hop/compute by segment:", [(round(ph[s].mean(), 2), round(pc[s].mean(), 2)) for s in seg])
+    # --- per-phase statistics over ALL tiles (time sixths of the pass) ---
+    if rep == reps - 1:
+        edges = np.linspace(0, done.max(), 7)
+        for s_ in range(6):
+            sel = (done >= edges[s_]) & (done < edges[s_ + 1] + (1e-9 if s_ == 5 else 0))
+            if not sel.any():
+                continue
+            lead = last_dep[sel] - grab[sel]          # > 0: grabbed before its last input was published
+            pp = prep[sel] - grab[sel]
+            late = (prep[sel] > last_dep[sel]).mean()
+            resid = done[sel] - grab[sel]
+            h2 = polled[sel] - np.maximum(last_dep[sel], prep[sel])
+            print(f"   sixth {s_}: {sel.sum()} tiles; grab->prep med {np.median(pp):.2f} p90 {np.percentile(pp,90):.2f}; "
+                  f"lead med {np.median(lead):.2f} p10 {np.percentile(lead,10):.2f}; prep-late frac {late:.2f}; "
+                  f"residency med {np.median(resid):.2f}; poll-after-max(dep,prep) med {np.median(h2):.2f} p90 {np.percentile(h2,90):.2f}")
+        # in-flight tiles over time
+        ts = np.linspace(0, done.max(), 13)[1:-1]
+        print("   in flight at t:", [(round(float(x), 0), int(((grab <= x) & (done > x)).sum())) for x in ts])
+        print("   waiting (prep done, not ready) at t:", [(round(float(x), 0), int(((prep <= x) & (polled > x)).sum())) for x in ts])
 np.save("/root/repo/gpurun_out/btile_trace.npy", tr)
