@@ -1207,7 +1207,7 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_trsv_ptile<true>, 256, out->smem);
     } else if (kn == "rpipe" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) {
       // one packed record per tile (dev::rp_layout), fetched by one TMA bulk copy
-      const dev::RpLayout lay = dev::rp_layout(rs, xs, (int)is, es, rps);
+      const dev::RpLayout lay = dev::rp_layout(rs, xs, dev::RP_INV, es, rps);
       std::vector<unsigned char> rec((size_t)nt * lay.bytes, 0);
 #pragma omp parallel for schedule(static)
       for (int t = 0; t < nt; ++t) {
@@ -1218,7 +1218,17 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
         std::memcpy(r + lay.o_rp, &rp[(size_t)t * rps], 2 * (size_t)rps);
         std::memcpy(r + lay.o_slot, &slot[(size_t)t * es], 2 * (size_t)es);
         std::memcpy(r + lay.o_val, &val[(size_t)t * es], 8 * (size_t)es);
-        std::memcpy(r + lay.o_inv, &inv[(size_t)t * is], 8 * (size_t)is);
+        // the inverse in the threads' order (dev::rp_inv_base): thread 4k + g, block j
+        // <- inv[k][g + 4j] of the packed column-major copy
+        double* iv = reinterpret_cast<double*>(r + lay.o_inv);
+        const int n_ = nr[t];
+        for (int j = 0; j < 16; ++j)
+          for (int th = 16 * j; th < 256; ++th) {
+            const int k = th >> 2, l = (th & 3) + 4 * j;
+            if (l <= k && k < n_)
+              iv[dev::rp_inv_base(j) - 16 * j + th] =
+                  inv[(size_t)t * is + (size_t)l * n_ - (size_t)l * (l - 1) / 2 + (k - l)];
+          }
       }
       CK(ctx, upload_vec(&out->rec, rec));
       out->recb = lay.bytes;

@@ -1383,6 +1383,12 @@ __global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
 // first poll loads are already in flight.  Deadlock-free like the other
 // in-order grabbers: a CTA finishes its tiles in grab order, so the smallest
 // unfinished tile is always some CTA's current one.
+// The record's inverse is stored in the threads' own order: block j (columns
+// l = g + 4j of every row slot k) holds the entries of threads tid >= 16j at
+// RP_INV_BASE(j) + tid - 16j, zeros where l > k or k >= rows, so a thread's 16
+// loads are conflict-free shared-memory reads at compile-time offsets.
+__host__ __device__ constexpr int rp_inv_base(int j) { return 256 * j - 8 * j * (j - 1); }
+constexpr int RP_INV = rp_inv_base(16);  // 2176 doubles
 struct RpLayout {
   int o_row, o_in, o_rp, o_slot, o_val, o_inv, bytes;
 };
@@ -1439,7 +1445,7 @@ __global__ void __launch_bounds__(256, 4)
   if (inactive(c)) return;
   extern __shared__ __align__(128) unsigned char rp_sm[];
   const int D = T.depth;
-  const RpLayout lay = rp_layout(T.rs, T.xs, T.is, T.es, T.rps);
+  const RpLayout lay = rp_layout(T.rs, T.xs, RP_INV, T.es, T.rps);
   double* ys = reinterpret_cast<double*>(rp_sm + (size_t)D * T.recb);  // RT_ROWS
   double* xin = ys + RT_ROWS;                                          // xs inputs, xin[xs] = 0
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(xin + T.xs + 2);
@@ -1473,7 +1479,9 @@ __global__ void __launch_bounds__(256, 4)
     unsigned nxt = 0;
     if (tid == 0) nxt = atomicAdd(&c.ctr[ctr_task], 1u);  // the slot's refill; used after barrier 2
     const unsigned char* buf = rp_sm + (size_t)s * T.recb;
+    if (trace && tid == 0) trace[8 * t + 7] = gtimer();  // rpipe: [7] = became the CTA's current tile
     mbar_wait(&mbar[s], (unsigned)(it / D) & 1u);
+    if (trace && tid == 0) trace[8 * t + 6] = gtimer();  // rpipe: [6] = record landed
     const int nr = *reinterpret_cast<const int*>(buf);
     const int* rowa = reinterpret_cast<const int*>(buf + lay.o_row);
     const int* ina = reinterpret_cast<const int*>(buf + lay.o_in);
@@ -1498,17 +1506,10 @@ __global__ void __launch_bounds__(256, 4)
     } else {
       b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
     }
-    // inverse entries inv[k][g+4j] (packed column-major: column l = rows l..nr-1
-    // at l*nr - l(l-1)/2) from the ring slot into registers
+    // inverse entries inv[k][g+4j] from the ring slot into registers
     double a[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int l = g + 4 * j;
-      const bool ok = (j <= jmax) && l <= k && k < nr;
-      const int idx = ok ? l * nr - ((l * (l - 1)) >> 1) + (k - l) : 0;
-      const double v = ib[idx];
-      a[j] = ok ? v : 0.0;
-    }
+    for (int j = 0; j < 16; ++j) a[j] = tid >= 16 * j ? ib[rp_inv_base(j) - 16 * j + tid] : 0.0;
     if (g == 0 && row >= 0) {  // sentinel resets folded into the pass (BD_FOLD_FILL)
       if (reset0) reset0[row] = __longlong_as_double(SENTINEL);
       if (reset1) reset1[row] = __longlong_as_double(SENTINEL);
@@ -1542,7 +1543,6 @@ __global__ void __launch_bounds__(256, 4)
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       if (g == 0) ys[k] = row >= 0 ? __dsub_rn(b, acc) : 0.0;
     }
-    if (trace && tid == 0) trace[8 * t + 6] = gtimer();
     __syncthreads();  // barrier 2: y in shared memory; the ring slot is free
     if (trace && tid == 0) trace[8 * t + 1] = gtimer();
     if (tid == 0) {
@@ -1565,7 +1565,6 @@ __global__ void __launch_bounds__(256, 4)
     if (trace && tid == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      trace[8 * t + 7] = gtimer();
       trace[8 * t + 2] = gtimer();
       trace[8 * t + 3] = ((unsigned long long)smid << 32) | blockIdx.x;
     }

@@ -100,6 +100,21 @@ for rep in range(reps):
             print(f"   sixth {s_}: {sel.sum()} tiles; grab->prep med {np.median(pp):.2f} p90 {np.percentile(pp,90):.2f}; "
                   f"lead med {np.median(lead):.2f} p10 {np.percentile(lead,10):.2f}; prep-late frac {late:.2f}; "
                   f"residency med {np.median(resid):.2f}; poll-after-max(dep,prep) med {np.median(h2):.2f} p90 {np.percentile(h2,90):.2f}")
+        if os.environ.get("BD_BTILE_KERNEL") == "rpipe":
+            top = densed  # rpipe records "became current" in slot 7
+            order_c = np.lexsort((top, tr[:, 3] & 0xffffffff))
+            cta = (tr[:, 3] & 0xffffffff)[order_c]
+            same = cta[1:] == cta[:-1]
+            gap = (top[order_c][1:] - done[order_c][:-1])[same]
+            mid = (done > done.max() / 3) & (done < 2 * done.max() / 3)
+            print("   rpipe mid-pass: mbar wait med %.2f p90 %.2f; landed->regs med %.2f p90 %.2f" % (
+                np.median((extd - top)[mid]), np.percentile((extd - top)[mid], 90),
+                np.median((prep - extd)[mid]), np.percentile((prep - extd)[mid], 90)))
+            print("   rpipe mid-pass: fetch issue->current med %.2f; current->regs loaded (mbar wait+LDS) med %.2f p90 %.2f; "
+                  "regs->polled med %.2f; polled->done med %.2f; current->done med %.2f; done->next current med %.2f" % (
+                      np.median((top - grab)[mid]), np.median((prep - top)[mid]), np.percentile((prep - top)[mid], 90),
+                      np.median((polled - prep)[mid]), np.median((done - polled)[mid]), np.median((done - top)[mid]),
+                      np.median(gap)))
         # in-flight tiles over time
         ts = np.linspace(0, done.max(), 13)[1:-1]
         print("   in flight at t:", [(round(float(x), 0), int(((grab <= x) & (done > x)).sum())) for x in ts])
