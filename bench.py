@@ -152,13 +152,13 @@ def assemble(wl, mode=None):
 
 def trsv_kernel():
     """Name of the triangular-solve kernel the library runs (BD_TRSV /
-    BD_BTILE_KERNEL knobs, defaults btile + reg -> k_trsv_rtile)."""
+    BD_BTILE_KERNEL knobs, defaults btile + auto -> k_trsv_rpipe)."""
     mode = os.environ.get("BD_TRSV", "btile")
     if mode != "btile":
         return f"trsv_{mode}"
     kern = os.environ.get("BD_BTILE_KERNEL", "auto")
-    return {"auto": "trsv_rtile", "reg": "trsv_rtile", "regt": "trsv_rtile", "rsmem": "trsv_rtile",
-            "pipe": "trsv_ptile"}.get(kern, "trsv_btile")
+    return {"auto": "trsv_rpipe", "rpipe": "trsv_rpipe", "reg": "trsv_rtile", "regt": "trsv_rtile",
+            "rsmem": "trsv_rtile", "pipe": "trsv_ptile"}.get(kern, "trsv_btile")
 
 
 def tri_bytes(nnz, rows):

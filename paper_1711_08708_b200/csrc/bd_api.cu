@@ -1190,7 +1190,9 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
         depth = std::max(depth, l + 1);
       }
       const double width = (double)nt / std::max(1, depth);
-      kn = width > 350.0 ? "rsmem" : "reg";
+      // k_trsv_rpipe (TMA ring) beats both in both regimes (cfg2 pair 379 -> 307 us,
+      // cfg3 1534 -> 1330 us); the others remain selectable
+      kn = (rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) ? "rpipe" : (width > 350.0 ? "rsmem" : "reg");
       if (getenv("BD_DEBUG"))
         std::fprintf(stderr, "[bd] btile auto: %d tiles, tile-DAG depth %d, %.0f tiles/level -> %s\n", nt,
                      depth, width, kn.c_str());
@@ -1256,6 +1258,13 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
         }
       }
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ps, 256, out->smem);
+      // the records hold everything the kernel reads: drop the separate arrays
+      // (task_row / tile_nr stay for the debug helpers)
+      cudaFree(out->inv), out->inv = nullptr;
+      cudaFree(out->ent_val), out->ent_val = nullptr;
+      cudaFree(out->ent_slot), out->ent_slot = nullptr;
+      cudaFree(out->ent_rp), out->ent_rp = nullptr;
+      cudaFree(out->in_col), out->in_col = nullptr;
     } else if (kn != "smem" && rs <= dev::RT_ROWS && xs <= 512 && ex <= 16) {
       out->reg = true;
       out->reg_smem = kn == "rsmem";
@@ -1581,7 +1590,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     // BD_FOLD_FILL: 1 = the forward pass resets the backward's output rows
     // (no fill before the backward); 2 = also the backward pass resets the
     // forward output it gathers (y_int stays sentinel between solves)
-    const int fold = (ib || !p->BL.reg || !p->BU.reg || p->rhs_pre) ? 0 : p->fold_fill;
+    const int fold = (ib || !p->BL.reg || !p->BU.reg) ? 0 : p->fold_fill;
     if (fold < 2) {
       dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
                                                                     dev::SENTINEL, c);
@@ -1591,7 +1600,7 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
                         //  the two passes alone are the triangular-solve class)
     if (!Rhs::kScalar && p->rhs_pre)
       TRY(launch_btile(p, p->BL, dev::RhsVec{p->rhs_pre, (int)p->n, nullptr, nullptr}, p->y_int, c,
-                       ctr0, ctr0 + 1, nullptr));
+                       ctr0, ctr0 + 1, nullptr, fold ? xg : nullptr));
     else
       TRY(launch_btile(p, p->BL, rhs, p->y_int, c, ctr0, ctr0 + 1, nullptr, fold ? xg : nullptr));
     prof_mark(ctx, p->prof_cls);

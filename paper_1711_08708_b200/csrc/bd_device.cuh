@@ -630,6 +630,17 @@ struct RhsVec {
     const double v = i < src_len ? src[i] : 0.0;
     return shift ? __dsub_rn(v, *shift) : v;
   }
+  // two-phase form (k_trsv_rpipe): the load goes out early and nothing uses it
+  // until the tile's inputs have landed, so the in-order warp does not stall on it
+  __device__ __forceinline__ double pass_const() const { return shift ? *shift : 0.0; }
+  __device__ __forceinline__ double load(int row) const {
+    if (row < 0) return 0.0;
+    const int i = perm ? perm[row] : row;
+    return i < src_len ? src[i] : 0.0;
+  }
+  __device__ __forceinline__ double finish(double v, double sh) const {
+    return shift ? __dsub_rn(v, sh) : v;
+  }
 };
 // w_i = r_v[i] - (S_i t)[i] with t = (t_raw - mt) + mu1/beta formed on the
 // fly: `rhs.v - stiff_intra @ t[:nh]` (bd/precond.py:307) fused with the

@@ -161,6 +161,9 @@ struct RhsGather {  // backward pass: the forward output
   __device__ __forceinline__ double eval(int row, int) const {
     return row < 0 ? 0.0 : src[row];
   }
+  __device__ __forceinline__ double pass_const() const { return 0.0; }
+  __device__ __forceinline__ double load(int row) const { return row < 0 ? 0.0 : src[row]; }
+  __device__ __forceinline__ double finish(double v, double) const { return v; }
 };
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -1472,6 +1475,8 @@ __global__ void __launch_bounds__(256, 4)
     }
   }
   __syncthreads();
+  double rhs_c = 0.0;  // per-pass constant of a scalar right-hand side (the mean shift)
+  if constexpr (Rhs::kScalar) rhs_c = rhs.pass_const();
   for (int it = 0;; ++it) {
     const int s = it % D;
     const int t = ids[s];
@@ -1502,7 +1507,7 @@ __global__ void __launch_bounds__(256, 4)
     }
     double b;
     if constexpr (Rhs::kScalar) {
-      b = rhs.template eval<1>(row, 0);
+      b = rhs.load(row);  // finished (mean shift) after the inputs have landed
     } else {
       b = rhs.template eval<4>(row, g);  // 4 consecutive lanes per row; valid in all four
     }
@@ -1541,6 +1546,7 @@ __global__ void __launch_bounds__(256, 4)
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if constexpr (Rhs::kScalar) b = rhs.finish(b, rhs_c);
       if (g == 0) ys[k] = row >= 0 ? __dsub_rn(b, acc) : 0.0;
     }
     __syncthreads();  // barrier 2: y in shared memory; the ring slot is free

@@ -15,7 +15,7 @@ from oracle import bidomain_oracle as orc  # noqa: E402
 from paper_1711_08708_b200 import configs  # noqa: E402
 from paper_1711_08708_b200.precond import regularize_stiffness  # noqa: E402
 
-KERNELS = ["auto", "reg", "rsmem", "regt", "pipe", "smem"]
+KERNELS = ["auto", "rpipe", "reg", "rsmem", "regt", "pipe", "smem"]
 
 
 @pytest.fixture(scope="module")

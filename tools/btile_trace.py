@@ -100,7 +100,7 @@ for rep in range(reps):
             print(f"   sixth {s_}: {sel.sum()} tiles; grab->prep med {np.median(pp):.2f} p90 {np.percentile(pp,90):.2f}; "
                   f"lead med {np.median(lead):.2f} p10 {np.percentile(lead,10):.2f}; prep-late frac {late:.2f}; "
                   f"residency med {np.median(resid):.2f}; poll-after-max(dep,prep) med {np.median(h2):.2f} p90 {np.percentile(h2,90):.2f}")
-        if os.environ.get("BD_BTILE_KERNEL") == "rpipe":
+        if os.environ.get("BD_BTILE_KERNEL", "auto") in ("rpipe", "auto"):
             top = densed  # rpipe records "became current" in slot 7
             order_c = np.lexsort((top, tr[:, 3] & 0xffffffff))
             cta = (tr[:, 3] & 0xffffffff)[order_c]
@@ -115,6 +115,32 @@ for rep in range(reps):
                       np.median((top - grab)[mid]), np.median((prep - top)[mid]), np.percentile((prep - top)[mid], 90),
                       np.median((polled - prep)[mid]), np.median((done - polled)[mid]), np.median((done - top)[mid]),
                       np.median(gap)))
+        if os.environ.get("BD_BTILE_KERNEL", "auto") in ("rpipe", "auto"):
+            # why do tiles become current late?  prev = the CTA's previous tile
+            top = densed
+            ctaid = tr[:, 3] & 0xffffffff
+            order_c = np.lexsort((top, ctaid))
+            prev = np.full(nt, -1)
+            same = ctaid[order_c][1:] == ctaid[order_c][:-1]
+            prev[order_c[1:][same]] = order_c[:-1][same]
+            mid = (done > done.max() / 3) & (done < 2 * done.max() / 3) & (prev >= 0)
+            late = top - last_dep           # > 0: became current after its last input was published
+            pw = (polled - top)[prev]       # how long the previous tile waited for its inputs
+            lm = mid & (late > 0)
+            print("   mid-pass: %d tiles, late %.2f; of the late ones: previous tile waited > 1.2 us: %.2f "
+                  "(median wait %.2f); late by med %.2f p90 %.2f" % (
+                      mid.sum(), lm.sum() / max(mid.sum(), 1), (pw[lm] > 1.2).mean(), np.median(pw[lm]),
+                      np.median(late[lm]), np.percentile(late[lm], 90)))
+            # level structure: spread of completion times within a tile level
+            lvl = bins.sum(1)
+            lv_done = np.array([[done[lvl == q].min(), np.median(done[lvl == q]), done[lvl == q].max()]
+                                for q in range(lvl.max() + 1)])
+            dl = np.diff(lv_done[:, 2])
+            print("   level max-done increments: first sixth %.2f, middle %.2f, last sixth %.2f; "
+                  "spread (max-min) in the middle %.2f" % (
+                      np.median(dl[: len(dl) // 6]), np.median(dl[len(dl) // 3: 2 * len(dl) // 3]),
+                      np.median(dl[-len(dl) // 6:]),
+                      np.median((lv_done[:, 2] - lv_done[:, 0])[len(dl) // 3: 2 * len(dl) // 3])))
         # in-flight tiles over time
         ts = np.linspace(0, done.max(), 13)[1:-1]
         print("   in flight at t:", [(round(float(x), 0), int(((grab <= x) & (done > x)).sum())) for x in ts])

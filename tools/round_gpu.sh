@@ -9,5 +9,5 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log
 BD_NO_GRAPH=1 python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_profile_step.log 2>&1 && \
 BD_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none -s 1000 -c 600 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_ncu_launch.log 2>&1
-BD_NO_GRAPH=1 ncu --set full --clock-control none --import-source on -k regex:k_trsv_rtile -s 600 -c 6 \
-  -o gpurun_out/${TAG}_rtile_full -f python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
+BD_NO_GRAPH=1 ncu --set full --clock-control none --import-source on -k regex:k_trsv_rpipe -s 600 -c 6 \
+  -o gpurun_out/${TAG}_rpipe_full -f python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
