@@ -1459,7 +1459,11 @@ __global__ void __launch_bounds__(256, 4)
   const int k = warp * 8 + (lane >> 2);  // row slot
   const int g = lane & 3;                // column group
   const int jmax = (8 * warp + 7) >> 2;  // warp-uniform: columns beyond the warp's rows are zero
-  unsigned long long* trace = g_tile_trace;
+  // trace selector (bd_debug_tile_trace steps): 1 = backward passes only, 2 = forward only
+  constexpr bool kBackward = Rhs::kScalar && sizeof(Rhs) == sizeof(RhsGather);
+  unsigned long long* trace =
+      (g_tile_trace_steps == 1 && !kBackward) || (g_tile_trace_steps == 2 && kBackward) ? nullptr
+                                                                                        : g_tile_trace;
   if (tid == 0) {
     xin[T.xs] = 0.0;
     for (int s = 0; s < D; ++s) mbar_init(&mbar[s], 1);
