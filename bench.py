@@ -345,9 +345,9 @@ def run_native(args, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": solve_bytes,
                          "note": ("latency-bound: the pass follows the tile DAG (81 tiles deep at "
                                   "cfg2); DRAM traffic is ~3x the algorithmic bytes because every "
-                                  "64-row tile streams its dense 16.6 KB diagonal-block inverse, "
-                                  "which timing experiments show is off the critical path "
-                                  "(DESIGN.md section 3)"),
+                                  "64-row tile streams a 19.8 KB record holding the dense inverse "
+                                  "of its diagonal block (one TMA bulk copy into a shared-memory "
+                                  "ring, off the critical path; DESIGN.md section 3)"),
                          "avg_launch_ms": round(bulk_ms, 5),
                          "levels": info_b["levels"],
                          "iteration": {"bytes": b_iter, "ms": round(ms_per_iter, 4),
