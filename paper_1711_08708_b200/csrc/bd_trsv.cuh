@@ -1555,13 +1555,6 @@ __global__ void __launch_bounds__(256, 4)
     }
     __syncthreads();  // barrier 2: y in shared memory; the ring slot is free
     if (trace && tid == 0) trace[8 * t + 1] = gtimer();
-    if (tid == 0) {
-      ids[s] = (int)nxt;  // read at the top of iteration it + D (D >= 2: a barrier in between)
-      if ((int)nxt < T.ntiles) {
-        tma_fetch(rp_sm + (size_t)s * T.recb, T.rec + (size_t)nxt * T.recb, (unsigned)T.recb, &mbar[s]);
-        if (trace) trace[8 * (size_t)nxt] = gtimer();
-      }
-    }
     {
       double sm[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -1571,6 +1564,15 @@ __global__ void __launch_bounds__(256, 4)
       x += __shfl_xor_sync(0xffffffffu, x, 1);
       x += __shfl_xor_sync(0xffffffffu, x, 2);
       if (g == 0 && row >= 0) publish(&xg[row], x);
+    }
+    // refill the slot (free since barrier 2) once this thread's rows are published, so the
+    // copy's set-up does not delay them
+    if (tid == 0) {
+      ids[s] = (int)nxt;  // read at the top of iteration it + D (D >= 2: a barrier in between)
+      if ((int)nxt < T.ntiles) {
+        tma_fetch(rp_sm + (size_t)s * T.recb, T.rec + (size_t)nxt * T.recb, (unsigned)T.recb, &mbar[s]);
+        if (trace) trace[8 * (size_t)nxt] = gtimer();
+      }
     }
     if (trace && tid == 0) {
       unsigned smid;
