@@ -166,6 +166,7 @@ struct DevBTile {
   bool tile_rhs = false;  // k_trsv_rtile with the right-hand side pre-gathered in tile order
   bool reg_smem = false;  // k_trsv_rtile with the inverse staged in shared memory
   bool rpipe = false;     // k_trsv_rpipe: packed per-tile records through a TMA ring
+  bool rpipe_wide = false;  // BD_RPIPE_WIDE=1: force the two-inputs-per-thread instantiation (tests)
   unsigned char* rec = nullptr;
   int recb = 0, depth = 2;
   dev::BTileDev dev() const {
@@ -1237,11 +1238,15 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       out->depth = std::max(2, std::min(8, getenv("BD_RPIPE_DEPTH") ? atoi(getenv("BD_RPIPE_DEPTH")) : 2));
       out->reg = true;
       out->rpipe = true;
+      out->rpipe_wide = getenv("BD_RPIPE_WIDE") && atoi(getenv("BD_RPIPE_WIDE")) != 0;
       out->threads = 256;
       out->smem = dev::rp_smem(out->recb, out->depth, xs);
-      auto pg = dev::k_trsv_rpipe<dev::RhsGather>;
-      auto pv = dev::k_trsv_rpipe<dev::RhsVec>;
-      auto ps = dev::k_trsv_rpipe<dev::RhsSchur>;
+      auto pg = dev::k_trsv_rpipe<false, dev::RhsGather>;
+      auto pv = dev::k_trsv_rpipe<false, dev::RhsVec>;
+      auto ps = dev::k_trsv_rpipe<false, dev::RhsSchur>;
+      auto wg = dev::k_trsv_rpipe<true, dev::RhsGather>;
+      auto wv = dev::k_trsv_rpipe<true, dev::RhsVec>;
+      auto ws = dev::k_trsv_rpipe<true, dev::RhsSchur>;
       {
         static std::mutex mu2;
         static size_t attr2[64] = {};
@@ -1254,6 +1259,9 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
           CK(ctx, cudaFuncSetAttribute(pg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           CK(ctx, cudaFuncSetAttribute(pv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           CK(ctx, cudaFuncSetAttribute(ps, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(wg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(wv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(ws, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           cur = out->smem;
         }
       }
@@ -1452,9 +1460,12 @@ bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* x
                        int ctr_task, int ctr_done, double* reset, double* r0 = nullptr,
                        double* r1 = nullptr) {
   bd_ctx* ctx = p->ctx;
-  if (b.rpipe && !reset)
-    dev::k_trsv_rpipe<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
-                                                                       ctr_done, r0, r1);
+  if (b.rpipe && !reset && (b.xs > 256 || b.rpipe_wide))
+    dev::k_trsv_rpipe<true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+                                                                             ctr_done, r0, r1);
+  else if (b.rpipe && !reset)
+    dev::k_trsv_rpipe<false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+                                                                              ctr_done, r0, r1);
   else if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
         b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);

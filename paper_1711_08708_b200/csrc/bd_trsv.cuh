@@ -1441,7 +1441,8 @@ __device__ __forceinline__ void tma_fetch(void* dst, const void* src, unsigned b
       : "memory");
 }
 
-template <class Rhs>
+// kWide: tiles with more than 256 inputs (two per thread)
+template <bool kWide, class Rhs>
 __global__ void __launch_bounds__(256, 4)
     k_trsv_rpipe(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
                  double* reset0 = nullptr, double* reset1 = nullptr) {
@@ -1500,10 +1501,11 @@ __global__ void __launch_bounds__(256, 4)
     const double* ib = reinterpret_cast<const double*>(buf + lay.o_inv);
     const int row = k < nr ? rowa[k] : -1;
     // the tile's distinct inputs, one poller each: first loads go out now
-    int icol[2];
-    long long pv[2] = {0, 0};
+    constexpr int NH = kWide ? 2 : 1;
+    int icol[NH];
+    long long pv[NH] = {};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NH; ++h) {
       const int j = tid + h * nth;
       icol[h] = j < T.xs ? ina[j] : -1;
       if (icol[h] >= 0)
@@ -1525,7 +1527,7 @@ __global__ void __launch_bounds__(256, 4)
     }
     if (trace && tid == 0) trace[8 * t + 5] = gtimer();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NH; ++h) {
       if (icol[h] < 0) continue;
       const double* pj = &xg[icol[h]];
       long long v = pv[h];
