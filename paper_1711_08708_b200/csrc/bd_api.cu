@@ -1235,18 +1235,20 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
       }
       CK(ctx, upload_vec(&out->rec, rec));
       out->recb = lay.bytes;
-      out->depth = std::max(2, std::min(8, getenv("BD_RPIPE_DEPTH") ? atoi(getenv("BD_RPIPE_DEPTH")) : 2));
+      out->depth = 2;  // compile-time in the kernel (three slots measured no gain)
       out->reg = true;
       out->rpipe = true;
       out->rpipe_wide = getenv("BD_RPIPE_WIDE") && atoi(getenv("BD_RPIPE_WIDE")) != 0;
       out->threads = 256;
       out->smem = dev::rp_smem(out->recb, out->depth, xs);
-      auto pg = dev::k_trsv_rpipe<false, dev::RhsGather>;
-      auto pv = dev::k_trsv_rpipe<false, dev::RhsVec>;
-      auto ps = dev::k_trsv_rpipe<false, dev::RhsSchur>;
-      auto wg = dev::k_trsv_rpipe<true, dev::RhsGather>;
-      auto wv = dev::k_trsv_rpipe<true, dev::RhsVec>;
-      auto ws = dev::k_trsv_rpipe<true, dev::RhsSchur>;
+      auto pg = dev::k_trsv_rpipe<false, false, dev::RhsGather>;
+      auto pv = dev::k_trsv_rpipe<false, false, dev::RhsVec>;
+      auto ps = dev::k_trsv_rpipe<false, false, dev::RhsSchur>;
+      auto wg = dev::k_trsv_rpipe<true, false, dev::RhsGather>;
+      auto wv = dev::k_trsv_rpipe<true, false, dev::RhsVec>;
+      auto ws = dev::k_trsv_rpipe<true, false, dev::RhsSchur>;
+      auto tg = dev::k_trsv_rpipe<false, true, dev::RhsGather>;
+      auto tv = dev::k_trsv_rpipe<false, true, dev::RhsVec>;
       {
         static std::mutex mu2;
         static size_t attr2[64] = {};
@@ -1262,6 +1264,8 @@ bd_status upload_btile(bd_ctx* ctx, const BTileSchedule& bs, DevBTile* out) {
           CK(ctx, cudaFuncSetAttribute(wg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           CK(ctx, cudaFuncSetAttribute(wv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           CK(ctx, cudaFuncSetAttribute(ws, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(tg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          CK(ctx, cudaFuncSetAttribute(tv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           cur = out->smem;
         }
       }
@@ -1455,17 +1459,24 @@ bd_status setup_btile(bd_inner* p, const HostCsr& lower, const HostCsr& upper,
   return BD_OK;
 }
 
+static bool g_tile_trace_on = false;  // bd_debug_tile_trace set a buffer: launch the tracing instantiation
+
 template <class Rhs>
 bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr_task, int ctr_done, double* reset, double* r0 = nullptr,
                        double* r1 = nullptr) {
   bd_ctx* ctx = p->ctx;
   if (b.rpipe && !reset && (b.xs > 256 || b.rpipe_wide))
-    dev::k_trsv_rpipe<true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
-                                                                             ctr_done, r0, r1);
-  else if (b.rpipe && !reset)
-    dev::k_trsv_rpipe<false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
-                                                                              ctr_done, r0, r1);
+    dev::k_trsv_rpipe<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
+  else if (b.rpipe && !reset && g_tile_trace_on && Rhs::kScalar) {
+    // per-tile timestamps (tools/btile_trace.py): scalar right-hand sides only
+    if constexpr (Rhs::kScalar)
+      dev::k_trsv_rpipe<false, true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+          b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
+  } else if (b.rpipe && !reset)
+    dev::k_trsv_rpipe<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+        b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
   else if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
         b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
@@ -2571,6 +2582,7 @@ bd_status bd_inner_apply(bd_inner* p, const double* y, double* z) {
 // Debug: enable the tiled-solve step trace (buffer of parts*steps*3 u64 on the
 // device; NULL disables).  Not part of the public header.
 bd_status bd_debug_tile_trace(void* dev_buf, int steps) {
+  g_tile_trace_on = dev_buf != nullptr;
   cudaMemcpyToSymbol(dev::g_tile_trace, &dev_buf, sizeof(void*));
   cudaMemcpyToSymbol(dev::g_tile_trace_steps, &steps, sizeof(int));
   return cudaGetLastError() == cudaSuccess ? BD_OK : BD_ECUDA;

@@ -1441,14 +1441,15 @@ __device__ __forceinline__ void tma_fetch(void* dst, const void* src, unsigned b
       : "memory");
 }
 
-// kWide: tiles with more than 256 inputs (two per thread)
-template <bool kWide, class Rhs>
+// kWide: tiles with more than 256 inputs (two per thread); kTrace: per-tile
+// timestamps for tools/btile_trace.py (launched only while a trace buffer is set)
+template <bool kWide, bool kTrace, class Rhs>
 __global__ void __launch_bounds__(256, 4)
     k_trsv_rpipe(BTileDev T, Rhs rhs, double* __restrict__ xg, Ctl c, int ctr_task, int ctr_done,
                  double* reset0 = nullptr, double* reset1 = nullptr) {
   if (inactive(c)) return;
   extern __shared__ __align__(128) unsigned char rp_sm[];
-  const int D = T.depth;
+  constexpr int D = 2;  // ring slots (three measured no gain and cost a CTA per SM)
   const RpLayout lay = rp_layout(T.rs, T.xs, RP_INV, T.es, T.rps);
   double* ys = reinterpret_cast<double*>(rp_sm + (size_t)D * T.recb);  // RT_ROWS
   double* xin = ys + RT_ROWS;                                          // xs inputs, xin[xs] = 0
@@ -1462,9 +1463,11 @@ __global__ void __launch_bounds__(256, 4)
   const int jmax = (8 * warp + 7) >> 2;  // warp-uniform: columns beyond the warp's rows are zero
   // trace selector (bd_debug_tile_trace steps): 1 = backward passes only, 2 = forward only
   constexpr bool kBackward = Rhs::kScalar && sizeof(Rhs) == sizeof(RhsGather);
-  unsigned long long* trace =
-      (g_tile_trace_steps == 1 && !kBackward) || (g_tile_trace_steps == 2 && kBackward) ? nullptr
-                                                                                        : g_tile_trace;
+  unsigned long long* trace = nullptr;
+  if constexpr (kTrace)
+    trace = (g_tile_trace_steps == 1 && !kBackward) || (g_tile_trace_steps == 2 && kBackward) ? nullptr
+                                                                                            : g_tile_trace;
+  (void)kBackward;
   if (tid == 0) {
     xin[T.xs] = 0.0;
     for (int s = 0; s < D; ++s) mbar_init(&mbar[s], 1);

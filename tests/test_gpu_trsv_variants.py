@@ -48,15 +48,13 @@ def test_tile_kernel_matches_oracle(problems, name, kernel, inbox, monkeypatch, 
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("depth,wide", [("2", "1"), ("3", "0"), ("3", "1")])
 @pytest.mark.parametrize("name", ["slab", "torso"])
-def test_ring_kernel_options_match_oracle(problems, name, depth, wide, monkeypatch, rng):
-    """k_trsv_rpipe with three ring slots and with the two-inputs-per-thread
-    instantiation (tiles with more than 256 inputs) forced."""
+def test_ring_kernel_wide_matches_oracle(problems, name, monkeypatch, rng):
+    """k_trsv_rpipe with the two-inputs-per-thread instantiation (tiles with more
+    than 256 inputs) forced."""
     monkeypatch.setenv("BD_TRSV", "btile")
     monkeypatch.setenv("BD_BTILE_KERNEL", "rpipe")
-    monkeypatch.setenv("BD_RPIPE_DEPTH", depth)
-    monkeypatch.setenv("BD_RPIPE_WIDE", wide)
+    monkeypatch.setenv("BD_RPIPE_WIDE", "1")
     g, xyz, ref = problems[name]
     ic = bd.IncompleteCholesky0()
     ic.setup(g, coords=xyz)
