@@ -211,6 +211,7 @@ struct bd_inner {
   bool btile = false;
   DevBTile BL, BU;
   double* rtmp = nullptr;
+  bool prefilled = false;     // the caller's previous kernel reset y_int (consumed by the next solve)
   double* rhs_pre = nullptr;  // btile: pre-evaluated non-scalar right-hand side
   double* rext = nullptr;  // supernodal forward: precomputed external phases (n)
   double* dense = nullptr; // exact inner, small n: explicit inverse (P A P^T)^{-1}, row-major
@@ -1613,7 +1614,9 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     // (no fill before the backward); 2 = also the backward pass resets the
     // forward output it gathers (y_int stays sentinel between solves)
     const int fold = (ib || !p->BL.reg || !p->BU.reg) ? 0 : p->fold_fill;
-    if (fold < 2) {
+    const bool prefilled = p->prefilled;  // y_int was reset by the kernel just before this solve
+    p->prefilled = false;
+    if (fold < 2 && !prefilled) {
       dev::k_fill<<<grid_for(ctx, nf1, dev::TPB), dev::TPB, 0, st>>>(ib ? p->inbox : p->y_int, nf1,
                                                                     dev::SENTINEL, c);
       LAUNCHED(ctx);
@@ -1829,19 +1832,31 @@ bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, c
   return BD_OK;
 }
 
+// The polled forward output of an inner's blocked-tile solve, if the kernel
+// right before that solve may reset it (BD_PREFILL=0 keeps the separate fill).
+double* fill_target(bd_inner* p) {
+  static const bool on = !(getenv("BD_PREFILL") && atoi(getenv("BD_PREFILL")) == 0);
+  if (!on || !p->btile || p->BL.inbox || !p->BL.reg || !p->BU.reg || p->fold_fill >= 2) return nullptr;
+  return p->y_int;
+}
+
 bd_status launch_corr(bd_prec* p, const double* s, const Ctl& c) {
   bd_ctx* ctx = p->sys->ctx;
   bd_system* sy = p->sys;
   if (sy->ell_w && !getenv("BD_NO_CORR_ELL")) {
     const dev::LamEll L{sy->ell_col, sy->ell_v1, sy->ell_v2};
     const int grid = grid_for(ctx, sy->m, dev::TPB);
+    // the second bulk solve follows: its forward output is reset here
+    double* ft = fill_target(p->bulk);
+    const int64_t nf = ft ? p->bulk->n : 0;
     switch (sy->ell_w) {
-      case 8: dev::k_corr_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
-      case 16: dev::k_corr_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
-      case 24: dev::k_corr_ell<24><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
-      default: dev::k_corr_ell<32><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n); break;
+      case 8: dev::k_corr_ell<8><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n, ft, nf); break;
+      case 16: dev::k_corr_ell<16><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n, ft, nf); break;
+      case 24: dev::k_corr_ell<24><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n, ft, nf); break;
+      default: dev::k_corr_ell<32><<<grid, dev::TPB, 0, ctx->stream>>>(L, (int)sy->n, (int)sy->m, s, p->corr, c, sy->n, ft, nf); break;
     }
     LAUNCHED(ctx);
+    if (ft) p->bulk->prefilled = true;
     return BD_OK;
   }
   {
@@ -1953,9 +1968,11 @@ bd_status enqueue_iteration(bd_prec* p) {
   const Ctl& c = p->ctl;
   TRY(launch_lambda(s, p->d, p->q, c, 1));
   prof_mark(ctx, 0);
+  double* ft = fill_target(p->bulk);  // the first bulk solve follows: its forward output is reset here
   dev::k_update<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->x, p->r, p->d, p->q, n,
-                                                                           nm, c);
+                                                                           nm, c, ft, ft ? p->bulk->n : 0);
   LAUNCHED(ctx);
+  if (ft) p->bulk->prefilled = true;
   prof_mark(ctx, 1);
   TRY(enqueue_pinv(p, p->r, p->z, p->z + n, nullptr, c, true));  // rho in its tail
   dev::k_dupdate<<<grid_for(ctx, nm, dev::TPB), dev::TPB, 0, ctx->stream>>>(p->z, p->d, n, nm, c);

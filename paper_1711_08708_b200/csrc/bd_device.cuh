@@ -594,14 +594,20 @@ __global__ void __launch_bounds__(TPB) k_init_res(const double* b, const double*
 }
 
 // x += αd ; r -= αq ; ||r||^2 ; sum(r_u)   (bd/krylov.py:109-123)
+// `fill` (optional): the polled forward output of the bulk inner solve that
+// follows, reset to the sentinel in the same pass (saves that solve's k_fill
+// launch; the lines are still L2-resident when the pass polls them).
 __global__ void __launch_bounds__(TPB) k_update(double* x, double* r, const double* d,
-                                                const double* q, int64_t n, int64_t nm, Ctl c) {
+                                                const double* q, int64_t n, int64_t nm, Ctl c,
+                                                double* __restrict__ fill = nullptr,
+                                                int64_t nfill = 0) {
   if (inactive(c)) return;
   __shared__ double sm[32];
   const double alpha = c.sc[S_ALPHA];
   double rr = 0.0, su = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm;
        i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nfill) fill[i] = __longlong_as_double(SENTINEL);
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, d[i]));
     const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
     r[i] = ri;

@@ -141,9 +141,14 @@ __global__ void __launch_bounds__(TPB) k_corr2(Csr si, const double* __restrict_
 // corr = S_i s on the ELL copy (thread per heart row), + its sum for mu2.
 template <int W>
 __global__ void __launch_bounds__(TPB) k_corr_ell(LamEll L, int n, int m, const double* __restrict__ s,
-                                                  double* __restrict__ corr, Ctl c, int64_t nmean) {
+                                                  double* __restrict__ corr, Ctl c, int64_t nmean,
+                                                  double* __restrict__ fill = nullptr,
+                                                  int64_t nfill = 0) {
   if (inactive(c)) return;
   __shared__ double sm[32];
+  // optional: reset the polled forward output of the bulk solve that follows (see k_update)
+  for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < nfill; i += (int64_t)gridDim.x * TPB)
+    fill[i] = __longlong_as_double(SENTINEL);
   double acc = 0.0;
   for (int r = blockIdx.x * TPB + threadIdx.x; r < m; r += gridDim.x * TPB) {
     double v = 0.0;
