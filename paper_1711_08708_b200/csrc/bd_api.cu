@@ -173,7 +173,7 @@ struct DevBTile {
     return dev::BTileDev{tile_nr, task_row, ent_rp,   ent_slot, ent_val, in_col, inv,
                          ntiles,  rs,       xs,       is,       es,      rps,    sleep_ns,
                          prefetch, poll_depth, inbox,    dst,      dmax,     exw,
-                         rec,     recb,     depth};
+                         rec,     recb,     depth,    INT32_MAX};
   }
 };
 
@@ -212,6 +212,9 @@ struct bd_inner {
   DevBTile BL, BU;
   double* rtmp = nullptr;
   bool prefilled = false;     // the caller's previous kernel reset y_int (consumed by the next solve)
+  double* post_fill = nullptr;  // polled forward output of the NEXT inner solve, reset by this solve's
+  int64_t post_fill_n = 0;      // backward pass (consumed by the next solve of this inner)
+  bd_inner* post_fill_owner = nullptr;
   double* rhs_pre = nullptr;  // btile: pre-evaluated non-scalar right-hand side
   double* rext = nullptr;  // supernodal forward: precomputed external phases (n)
   double* dense = nullptr; // exact inner, small n: explicit inverse (P A P^T)^{-1}, row-major
@@ -1465,27 +1468,29 @@ static bool g_tile_trace_on = false;  // bd_debug_tile_trace set a buffer: launc
 template <class Rhs>
 bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* xg, const Ctl& c,
                        int ctr_task, int ctr_done, double* reset, double* r0 = nullptr,
-                       double* r1 = nullptr) {
+                       double* r1 = nullptr, int64_t r1n = INT32_MAX) {
   bd_ctx* ctx = p->ctx;
+  dev::BTileDev T = b.dev();
+  T.reset1_n = (int)std::min<int64_t>(r1n, INT32_MAX);
   if (b.rpipe && !reset && (b.xs > 256 || b.rpipe_wide))
     dev::k_trsv_rpipe<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
+        T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
   else if (b.rpipe && !reset && g_tile_trace_on && Rhs::kScalar) {
     // per-tile timestamps (tools/btile_trace.py): scalar right-hand sides only
     if constexpr (Rhs::kScalar)
       dev::k_trsv_rpipe<false, true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-          b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
+          T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
   } else if (b.rpipe && !reset)
     dev::k_trsv_rpipe<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, r0, r1);
+        T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
   else if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
+        T, rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else if (b.reg && !reset)
     dev::k_trsv_rtile<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        b.dev(), rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
+        T, rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else
-    dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(b.dev(), rhs, xg, c, ctr_task,
+    dev::k_trsv_btile<Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(T, rhs, xg, c, ctr_task,
                                                                        ctr_done, reset);
   LAUNCHED(ctx);
   return BD_OK;
@@ -1635,8 +1640,15 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
       LAUNCHED(ctx);
     }
     prof_mark(ctx, 5);
-    TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr, nullptr,
-                     fold >= 2 ? p->y_int : nullptr));
+    {
+      double* pf = (fold < 2 && p->BU.reg) ? p->post_fill : nullptr;
+      const int64_t pfn = p->post_fill_n;
+      p->post_fill = nullptr;
+      TRY(launch_btile(p, p->BU, dev::RhsGather{p->y_int}, xg, c, ctr0 + 2, ctr0 + 3, nullptr, nullptr,
+                       fold >= 2 ? p->y_int : pf, fold >= 2 ? (int64_t)INT32_MAX : pfn));
+      if (pf && p->post_fill_owner) p->post_fill_owner->prefilled = true;
+      p->post_fill_owner = nullptr;
+    }
     prof_mark(ctx, p->prof_cls);
     if (fin >= 0) TRY(launch_dot(ctx, xg, nullptr, p->n, c, ctr0 + 1, fin, slot, slot2, nmean));
     prof_mark(ctx, 5);
@@ -1834,8 +1846,12 @@ bd_status launch_dot(bd_ctx* ctx, const double* x, const double* y, int64_t n, c
 
 // The polled forward output of an inner's blocked-tile solve, if the kernel
 // right before that solve may reset it (BD_PREFILL=0 keeps the separate fill).
+int prefill_level() {  // BD_PREFILL: 0 off, 1 bulk solves, 2 (default) + the Schur solve
+  static const int lv = getenv("BD_PREFILL") ? atoi(getenv("BD_PREFILL")) : 2;
+  return lv;
+}
 double* fill_target(bd_inner* p) {
-  static const bool on = !(getenv("BD_PREFILL") && atoi(getenv("BD_PREFILL")) == 0);
+  const bool on = prefill_level() >= 1;
   if (!on || !p->btile || p->BL.inbox || !p->BL.reg || !p->BU.reg || p->fold_fill >= 2) return nullptr;
   return p->y_int;
 }
@@ -1908,10 +1924,21 @@ bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, 
       xi = p->traw;
       out = nullptr;
     }
+    // the Schur solve follows directly (in the PCG no dot in between): the bulk solve's
+    // backward pass resets the Schur solve's polled forward output on its way
+    if (in_pcg && prefill_level() >= 2 && p->bulk != p->schur && p->bulk->btile && p->bulk->BU.rpipe) {
+      if (double* ft = fill_target(p->schur)) {
+        p->bulk->post_fill = ft;
+        p->bulk->post_fill_n = m;
+        p->bulk->post_fill_owner = p->schur;
+      }
+    }
     if (in_pcg)
       TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S));
     else
       TRY(inner_solve(p->bulk, rhs, xi, out, c, dev::C_BULK1_S, dev::FIN_MEAN, dev::S_MT, -1, n));
+    p->bulk->post_fill = nullptr;
+    p->bulk->post_fill_owner = nullptr;
   }
   prof_mark(ctx, 2);
   // s = K^{-1}(r_v - S_i t[:m])

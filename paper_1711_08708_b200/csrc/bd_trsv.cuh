@@ -925,6 +925,7 @@ struct BTileDev {
   const unsigned char* rec;
   int recb;                         // record stride in bytes (16-byte multiple)
   int depth;                        // ring slots per CTA (>= 2)
+  int reset1_n;                     // rows below this bound are reset through `reset1` (launch-time)
 };
 constexpr int BT_LANES = 4;  // lanes per row in the dense step
 
@@ -1267,7 +1268,7 @@ __global__ void __launch_bounds__(256, kSmemInv ? 8 : 4)
     // (the forward output, read above) for the inner's next forward pass
     if (g == 0 && row >= 0) {
       if (reset0) reset0[row] = __longlong_as_double(SENTINEL);
-      if (reset1) reset1[row] = __longlong_as_double(SENTINEL);
+      if (reset1 && row < T.reset1_n) reset1[row] = __longlong_as_double(SENTINEL);
     }
     if (trace) {
       __syncthreads();
@@ -1526,7 +1527,7 @@ __global__ void __launch_bounds__(256, 4)
     for (int j = 0; j < 16; ++j) a[j] = tid >= 16 * j ? ib[rp_inv_base(j) - 16 * j + tid] : 0.0;
     if (g == 0 && row >= 0) {  // sentinel resets folded into the pass (BD_FOLD_FILL)
       if (reset0) reset0[row] = __longlong_as_double(SENTINEL);
-      if (reset1) reset1[row] = __longlong_as_double(SENTINEL);
+      if (reset1 && row < T.reset1_n) reset1[row] = __longlong_as_double(SENTINEL);
     }
     if (trace && tid == 0) trace[8 * t + 5] = gtimer();
 #pragma unroll
