@@ -1610,10 +1610,32 @@ bd_status inner_solve_g(bd_inner* p, const Rhs& rhs, double* x_int, double* out,
     const bool ib = p->BL.inbox != nullptr;
     const int64_t nf1 = ib ? (int64_t)p->BL.ntiles * p->BL.xs : p->n;
     const int64_t nf2 = ib ? (int64_t)p->BU.ntiles * p->BU.xs : p->n;
-    if (!Rhs::kScalar && p->rhs_pre) {
-      dev::k_rhs_eval<G, Rhs><<<grid_for(ctx, p->n, dev::TPB / G), dev::TPB, 0, st>>>(
-          (int)p->n, rhs, p->rhs_pre, c);
-      LAUNCHED(ctx);
+    if constexpr (!Rhs::kScalar) {
+      if (p->rhs_pre) {
+        if (rhs.ell_w && !rhs.perm && rhs.si.nrows == p->n) {
+          const int grid = grid_for(ctx, p->n, dev::TPB);
+#define SCHUR_RHS_ELL(WW)                                                                          \
+  case WW:                                                                                         \
+    dev::k_schur_rhs_ell<WW><<<grid, dev::TPB, 0, st>>>(rhs.ell_col, rhs.ell_v2, rhs.ell_n,         \
+                                                        (int)p->n, rhs.traw, rhs.sc, rhs.rv,        \
+                                                        p->rhs_pre, c);                            \
+    break;
+          switch (rhs.ell_w) {
+            SCHUR_RHS_ELL(8)
+            SCHUR_RHS_ELL(16)
+            SCHUR_RHS_ELL(24)
+            default:
+              dev::k_schur_rhs_ell<32><<<grid, dev::TPB, 0, st>>>(rhs.ell_col, rhs.ell_v2, rhs.ell_n,
+                                                                  (int)p->n, rhs.traw, rhs.sc, rhs.rv,
+                                                                  p->rhs_pre, c);
+          }
+#undef SCHUR_RHS_ELL
+        } else {
+          dev::k_rhs_eval<G, Rhs><<<grid_for(ctx, p->n, dev::TPB / G), dev::TPB, 0, st>>>(
+              (int)p->n, rhs, p->rhs_pre, c);
+        }
+        LAUNCHED(ctx);
+      }
     }
     // BD_FOLD_FILL: 1 = the forward pass resets the backward's output rows
     // (no fill before the backward); 2 = also the backward pass resets the
@@ -1944,6 +1966,12 @@ bd_status enqueue_pinv(bd_prec* p, const double* r, double* zu, double* zv_int, 
   // s = K^{-1}(r_v - S_i t[:m])
   {
     dev::RhsSchur rhs{s->Si->dev(), p->traw, in_pcg ? p->zsc : c.sc, r + n, p->schur->perm};
+    if (s->ell_w && !getenv("BD_NO_CORR_ELL")) {  // the ELL copy for the streaming pre-evaluation
+      rhs.ell_col = s->ell_col;
+      rhs.ell_v2 = s->ell_v2;
+      rhs.ell_w = s->ell_w;
+      rhs.ell_n = (int)s->n;
+    }
     double* xi = zv_int;
     double* out = zv_out;
     if (p->schur->perm) {
@@ -2721,6 +2749,11 @@ bd_status bd_blocklu_create(bd_system* s, bd_inner* bulk, bd_inner* schur, doubl
                      cudaMemcpyDeviceToDevice));
   const char* env = getenv("BD_NO_GRAPH");
   p->use_graph = !(env && env[0] == '1');
+  // The Schur solve's right-hand side r_v - S_i t: evaluated by one streaming kernel on
+  // the ELL copy before the forward pass (BD_RHS_PRE=0: inside the pass's tiles)
+  if (!(getenv("BD_RHS_PRE") && atoi(getenv("BD_RHS_PRE")) == 0) && schur->btile && schur->BL.rpipe &&
+      !schur->rhs_pre && s->ell_w && !schur->perm)
+    if (dalloc(&schur->rhs_pre, m)) return fail(ctx, BD_ECUDA, "bd_blocklu_create: out of device memory");
   *out = p;
   return BD_OK;
 }

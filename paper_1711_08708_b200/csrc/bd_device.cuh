@@ -658,6 +658,11 @@ struct RhsSchur {
   const double* sc;
   const double* rv;
   const int* perm;
+  // optional: the entry-major ELL copy of S_i (LamEll::col / v2), for the streaming
+  // pre-evaluation k_schur_rhs_ell (ell_w = 0: none)
+  const int* ell_col = nullptr;
+  const double* ell_v2 = nullptr;
+  int ell_w = 0, ell_n = 0;
   template <int G>
   __device__ __forceinline__ double eval(int row, int lane) const {
     const int i = row < 0 ? -1 : (perm ? perm[row] : row);

@@ -173,6 +173,39 @@ __global__ void __launch_bounds__(TPB) k_corr_ell(LamEll L, int n, int m, const 
   reduce_tail<1>(c, vv, gridDim.x, blockIdx.x, C_CORR, FIN_MEAN, S_MU2, S_C2, nmean, sm);
 }
 
+// w = r_v - S_i t on the ELL copy (thread per heart row), t = (t_raw - mt) + c1 as in
+// RhsSchur: the Schur solve's right-hand side evaluated by one streaming kernel before
+// the forward pass, which then reads a plain vector (bd/precond.py:307).
+template <int W>
+__global__ void __launch_bounds__(TPB) k_schur_rhs_ell(const int* __restrict__ col,
+                                                       const double* __restrict__ v2, int n, int m,
+                                                       const double* __restrict__ traw,
+                                                       const double* __restrict__ sc,
+                                                       const double* __restrict__ rv,
+                                                       double* __restrict__ y, Ctl c) {
+  if (inactive(c)) return;
+  const double mt = sc[S_MT], c1 = sc[S_C1];
+  for (int r = blockIdx.x * TPB + threadIdx.x; r < m; r += gridDim.x * TPB) {
+    double v = 0.0;
+#pragma unroll
+    for (int e0 = 0; e0 < W; e0 += 8) {
+      int cl[8];
+      double a[8], xv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cl[e] = __ldg(&col[(size_t)(e0 + e) * n + r]);
+        a[e] = __ldg(&v2[(size_t)(e0 + e) * m + r]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        xv[e] = cl[e] < m ? __dadd_rn(__dsub_rn(__ldg(&traw[cl[e]]), mt), c1) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v = fma(a[e], xv[e], v);
+    }
+    y[r] = __dsub_rn(rv[r], v);
+  }
+}
+
 // z_u = t - bulk(corr) with both recentrings applied on the fly
 // (bd/precond.py:291-292, 311): the standalone P^{-1} (bd_blocklu_apply)
 __global__ void __launch_bounds__(TPB) k_combine(const double* __restrict__ traw,
