@@ -3312,8 +3312,13 @@ bd_status bd_shard_create(bd_ctx* ctx, int64_t n, int64_t m, int64_t n_global, b
   h->hist_cap = (int)std::max<int64_t>(hist_cap, 2);
   h->red = red;  // caller-owned (the host all-reduces slices of it in place)
   if (Si_ext && z1ext && Si_ext->nrows == m) {
-    h->Si_ext = Si_ext;
-    h->z1ext = z1ext;
+    h->z1ext = z1ext;  // z1 and its halo stay contiguous either way
+    // The Schur right-hand side r_v - S_i [z1 | ghosts]: with the TMA-ring tile kernel one
+    // streaming split SpMV before the pass beats the product inside its tiles (as on one
+    // GPU); BD_SHARD_RHS_PRE=0 keeps the in-tile RhsSchur on S_i's extended copy
+    const bool pre = schur->btile && schur->BL.rpipe && Si->ell_w &&
+                     !(getenv("BD_SHARD_RHS_PRE") && atoi(getenv("BD_SHARD_RHS_PRE")) == 0);
+    if (!pre) h->Si_ext = Si_ext;
   }
   const int64_t nm = n + m;
   bool bad = dalloc(&h->x, nm) || dalloc(&h->r, nm) || dalloc(&h->d, nm) || dalloc(&h->q, nm) ||
@@ -3415,6 +3420,7 @@ bd_status bd_shard_lambda(bd_shard* h, const double* v, const double* ug, const 
 bd_status bd_shard_init(bd_shard* h, const double* b, int has_x0) {
   if (!h || !b) return BD_EINVAL;
   bd_ctx* ctx = h->ctx;
+  h->bulk->prefilled = h->schur->prefilled = false;  // a new solve starts with explicit fills
   Scope sc(ctx);
   dev::k_sh_init<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->n + h->m, b, has_x0 ? h->q : nullptr,
                                                              h->r, h->Si_ext ? nullptr : h->rhs_s,
@@ -3443,11 +3449,14 @@ bd_status bd_shard_update(bd_shard* h) {
   Scope sc(ctx);
   dev::k_sh_alpha<<<1, 1, 0, ctx->stream>>>(h->sc, h->fl, h->si, h->red);
   LAUNCHED(ctx);
+  // the first bulk solve (bd_shard_pinv1) follows: its polled forward output is reset here
+  double* ft = fill_target(h->bulk);
   dev::k_sh_update<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(h->n, h->n + h->m, h->x, h->r, h->d, h->q,
                                                                h->Si_ext ? nullptr : h->rhs_s, h->sc,
                                                                h->part, h->ctr + 2,
-                                                               h->red + 1, h->fl);
+                                                               h->red + 1, h->fl, ft, ft ? h->n : 0);
   LAUNCHED(ctx);
+  if (ft) h->bulk->prefilled = true;
   return BD_OK;
 }
 
@@ -3456,7 +3465,19 @@ bd_status bd_shard_pinv1(bd_shard* h) {
   if (!h) return BD_EINVAL;
   Scope sc(h->ctx);
   dev::RhsVec rhs{h->r, (int)h->n, h->sc + dev::SH_MU1, h->bulk->perm};
-  return shard_inner(h->bulk, rhs, h->z1, h->cb);
+  // the Schur solve follows (halo gathers in between do not touch its buffers): the bulk
+  // solve's backward pass resets the Schur solve's polled forward output
+  if (prefill_level() >= 2 && h->m > 0 && h->bulk != h->schur && h->bulk->btile && h->bulk->BU.rpipe) {
+    if (double* ft = fill_target(h->schur)) {
+      h->bulk->post_fill = ft;
+      h->bulk->post_fill_n = h->m;
+      h->bulk->post_fill_owner = h->schur;
+    }
+  }
+  const bd_status st = shard_inner(h->bulk, rhs, h->z1, h->cb);
+  h->bulk->post_fill = nullptr;
+  h->bulk->post_fill_owner = nullptr;
+  return st;
 }
 
 // s = K^{-1}(r_v − S_i [z1 | tg]); with S_i's ghost columns at n + j and the
@@ -3482,10 +3503,12 @@ bd_status bd_shard_pinv3(bd_shard* h, const double* sg) {
   bd_ctx* ctx = h->ctx;
   if (h->m > 0 && h->Si->ell_w) {  // one pass: product and its sum
     Scope sc(ctx);
+    double* ft = fill_target(h->bulk);  // the second bulk solve (bd_shard_pinv4) follows
     dev::k_sh_corr_ell<<<dev::SH_GRID, dev::TPB, 0, ctx->stream>>>(
         h->m, h->Si->ell_w, h->Si->ell_col, h->Si->ell_val, h->s, sg, h->corr, h->part, h->ctr + 3,
-        h->red + 3, h->fl);
+        h->red + 3, h->fl, ft, ft ? h->n : 0);
     LAUNCHED(ctx);
+    if (ft) h->bulk->prefilled = true;
     return BD_OK;
   }
   if (h->m > 0) TRY(bd_spmv_split(h->Si, h->s, h->m, sg, h->corr, 1.0, 0.0));

@@ -172,8 +172,13 @@ __global__ void __launch_bounds__(TPB) k_sh_corr_ell(int64_t m, int w, const int
                                                      const double* __restrict__ s,
                                                      const double* __restrict__ sg,
                                                      double* __restrict__ corr, double* part,
-                                                     unsigned* ctr, double* red, const int* fl) {
+                                                     unsigned* ctr, double* red, const int* fl,
+                                                     double* __restrict__ fill = nullptr,
+                                                     int64_t nfill = 0) {
   if (sh_done(fl)) return;
+  // optional: sentinel reset of the polled forward output of the bulk solve that follows
+  for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < nfill; i += (int64_t)gridDim.x * TPB)
+    fill[i] = __longlong_as_double(SENTINEL);
   double acc[1] = {0.0};
   for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < m; i += (int64_t)gridDim.x * TPB) {
     double v = 0.0;
@@ -233,11 +238,14 @@ __global__ void k_sh_alpha(double* sc, int* fl, int* si, const double* red) {
 __global__ void __launch_bounds__(TPB) k_sh_update(int64_t n, int64_t nm, double* x, double* r,
                                                    const double* d, const double* q,
                                                    double* rhs_s, const double* sc, double* part,
-                                                   unsigned* ctr, double* red2, const int* fl) {
+                                                   unsigned* ctr, double* red2, const int* fl,
+                                                   double* __restrict__ fill = nullptr,
+                                                   int64_t nfill = 0) {
   if (sh_done(fl)) return;
   const double a = sc[SH_ALPHA];
   double acc[2] = {0.0, 0.0};
   for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < nm; i += (int64_t)gridDim.x * TPB) {
+    if (i < nfill) fill[i] = __longlong_as_double(SENTINEL);  // the next bulk solve's polled output
     x[i] = fma(a, d[i], x[i]);
     const double ri = fma(-a, q[i], r[i]);
     r[i] = ri;
