@@ -1480,10 +1480,32 @@ bd_status launch_btile(bd_inner* p, const DevBTile& b, const Rhs& rhs, double* x
     if constexpr (Rhs::kScalar)
       dev::k_trsv_rpipe<false, true, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
           T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
-  } else if (b.rpipe && !reset)
-    dev::k_trsv_rpipe<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
-        T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
-  else if (b.reg && b.reg_smem && !reset)
+  } else if (b.rpipe && !reset) {
+    // The polled output vector as a persisting L2 window (BD_L2_PERSIST=0: off), so the
+    // record stream (400 MB per pass) does not evict the lines the tiles spin on
+    static const int persist = getenv("BD_L2_PERSIST") ? atoi(getenv("BD_L2_PERSIST")) : 1;
+    if (persist) {
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = xg;
+      at[0].val.accessPolicyWindow.num_bytes = sizeof(double) * (size_t)p->n;
+      at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaLaunchConfig_t cf = {};
+      cf.gridDim = dim3(b.grid);
+      cf.blockDim = dim3(b.threads);
+      cf.dynamicSmemBytes = b.smem;
+      cf.stream = ctx->stream;
+      cf.attrs = at;
+      cf.numAttrs = 1;
+      CK(ctx, cudaLaunchKernelEx(&cf, dev::k_trsv_rpipe<false, false, Rhs>, T, rhs, xg, c, ctr_task, ctr_done,
+                                 r0, r1));
+    } else {
+      dev::k_trsv_rpipe<false, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
+          T, rhs, xg, c, ctr_task, ctr_done, r0, r1);
+    }
+  } else if (b.reg && b.reg_smem && !reset)
     dev::k_trsv_rtile<true, false, Rhs><<<b.grid, b.threads, b.smem, ctx->stream>>>(
         T, rhs, xg, c, ctr_task, ctr_done, nullptr, nullptr, nullptr, r0, r1);
   else if (b.reg && !reset)
@@ -2100,6 +2122,15 @@ bd_status bd_ctx_create(int device, void* stream, bd_ctx** out) {
     return BD_ECUDA;
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  // L2 set-aside for the persisting window of the triangular passes' polled vectors
+  // (launch_btile; the limit cannot be set during graph capture)
+  if (!(getenv("BD_L2_PERSIST") && atoi(getenv("BD_L2_PERSIST")) == 0)) {
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    if (max_persist > 0)
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)max_persist, (size_t)48 << 20));
+    cudaGetLastError();
+  }
   c->user = (cudaStream_t)stream;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
