@@ -1432,13 +1432,17 @@ __device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
   } while (!ok);
 }
 // one elected thread: arm the slot's barrier with the byte count and start the copy
+// The records are read once per pass and never again before 400 MB more have gone by:
+// fetched with an evict-first L2 policy so they do not push out the vectors the tiles poll.
 __device__ __forceinline__ void tma_fetch(void* dst, const void* src, unsigned bytes, void* bar) {
   const unsigned b = smem_u32(bar);
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(b)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+      "[%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(b), "l"(pol)
       : "memory");
 }
 
