@@ -464,9 +464,11 @@ __global__ void __launch_bounds__(TPB) k_lambda_ell(LamEll L, const double* __re
       double a1[8], a2[8], xu[8], xv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        cl[e] = __ldg(&L.col[(size_t)(e0 + e) * n + row]);
-        a1[e] = __ldg(&L.v1[(size_t)(e0 + e) * n + row]);
-        a2[e] = h ? __ldg(&L.v2[(size_t)(e0 + e) * m + row]) : 0.0;
+        // matrix entries are read once per apply: streaming (evict-first) loads keep the
+        // vectors of the neighbouring kernels in L2
+        cl[e] = __ldcs(&L.col[(size_t)(e0 + e) * n + row]);
+        a1[e] = __ldcs(&L.v1[(size_t)(e0 + e) * n + row]);
+        a2[e] = h ? __ldcs(&L.v2[(size_t)(e0 + e) * m + row]) : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) {

@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(TPB) k_corr_ell(LamEll L, int n, int m, const 
       double a[8], xv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        cl[e] = __ldg(&L.col[(size_t)(e0 + e) * n + r]);
-        a[e] = __ldg(&L.v2[(size_t)(e0 + e) * m + r]);
+        cl[e] = __ldcs(&L.col[(size_t)(e0 + e) * n + r]);
+        a[e] = __ldcs(&L.v2[(size_t)(e0 + e) * m + r]);
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) xv[e] = cl[e] < m ? __ldg(&s[cl[e]]) : 0.0;
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(TPB) k_schur_rhs_ell(const int* __restrict__ c
       double a[8], xv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        cl[e] = __ldg(&col[(size_t)(e0 + e) * n + r]);
-        a[e] = __ldg(&v2[(size_t)(e0 + e) * m + r]);
+        cl[e] = __ldcs(&col[(size_t)(e0 + e) * n + r]);
+        a[e] = __ldcs(&v2[(size_t)(e0 + e) * m + r]);
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e)
