@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(TPB) k_sh_lambda_ell(
       double a[8], xv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        cl[e] = __ldg(&c1[(int64_t)(e0 + e) * n + i]);
-        a[e] = __ldg(&a1[(int64_t)(e0 + e) * n + i]);
+        cl[e] = __ldcs(&c1[(int64_t)(e0 + e) * n + i]);  // matrix entries: streaming loads
+        a[e] = __ldcs(&a1[(int64_t)(e0 + e) * n + i]);
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) xv[e] = cl[e] < 0 ? 0.0 : (cl[e] < n ? __ldg(&x[cl[e]]) : __ldg(&ug[cl[e] - n]));
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(TPB) k_sh_lambda_ell(
         double a[8], xv[8], xu[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          cl[e] = __ldg(&c2[(int64_t)(e0 + e) * m + i]);
-          a[e] = __ldg(&a2[(int64_t)(e0 + e) * m + i]);
+          cl[e] = __ldcs(&c2[(int64_t)(e0 + e) * m + i]);
+          a[e] = __ldcs(&a2[(int64_t)(e0 + e) * m + i]);
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(TPB) k_sh_corr_ell(int64_t m, int w, const int
       double a[8], xv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        cl[e] = __ldg(&c2[(int64_t)(e0 + e) * m + i]);
-        a[e] = __ldg(&a2[(int64_t)(e0 + e) * m + i]);
+        cl[e] = __ldcs(&c2[(int64_t)(e0 + e) * m + i]);
+        a[e] = __ldcs(&a2[(int64_t)(e0 + e) * m + i]);
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) xv[e] = cl[e] < 0 ? 0.0 : (cl[e] < m ? __ldg(&s[cl[e]]) : __ldg(&sg[cl[e] - m]));
